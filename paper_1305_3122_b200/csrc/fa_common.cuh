@@ -1,0 +1,154 @@
+// Shared device/host helpers for the femasm_b200 library (sm_100a).
+#pragma once
+
+#include <cstdint>
+#include <cstdio>
+#include <cuda_runtime.h>
+
+#include "../../include/femasm_b200.h"
+
+namespace fa {
+
+constexpr double AREA_EPS = 1e-300;  // mesh.py:27 (AREA_EPS)
+constexpr int NUM_SMS_B200 = 148;
+
+// ---- host-side error state -------------------------------------------------------------
+void set_error(const char* fmt, ...);
+int cuda_status(cudaError_t e, const char* what);
+
+#define FA_CUDA(call)                                                      \
+    do {                                                                   \
+        cudaError_t _e = (call);                                           \
+        if (_e != cudaSuccess) return ::fa::cuda_status(_e, #call);        \
+    } while (0)
+
+#define FA_LAUNCH_CHECK(what)                                              \
+    do {                                                                   \
+        cudaError_t _e = cudaGetLastError();                               \
+        if (_e != cudaSuccess) return ::fa::cuda_status(_e, what);         \
+    } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int grid_for(int64_t n, int block, int per_sm = 8) {
+    int64_t want = (n + block - 1) / block;
+    int64_t cap = int64_t(NUM_SMS_B200) * per_sm;
+    if (want > cap) want = cap;
+    if (want < 1) want = 1;
+    return int(want);
+}
+
+// ---- device helpers ----------------------------------------------------------------------
+__device__ __forceinline__ void atomic_min_i64(int64_t* addr, int64_t v) {
+    atomicMin(reinterpret_cast<long long*>(addr), static_cast<long long>(v));
+}
+
+__device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_volatile_u64(uint64_t* p, uint64_t v) {
+    asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Streaming (read-once) loads: keep them from evicting the gathered working set in L2.
+__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
+    uint32_t v;
+    asm volatile("ld.global.L1::no_allocate.L2::evict_first.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_inclusive_scan(T v) {
+    const int lane = threadIdx.x & 31;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        T o = __shfl_up_sync(0xffffffffu, v, d);
+        if (lane >= d) v += o;
+    }
+    return v;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    return v;
+}
+
+// Block-wide exclusive scan of one value per thread.  Returns the exclusive prefix of the
+// calling thread; *total receives the block aggregate.  `warp_tot` is shared scratch of
+// BLOCK/32 entries.
+template <int BLOCK, typename T>
+__device__ __forceinline__ T block_exclusive_scan(T v, T* warp_tot, T* total) {
+    constexpr int NW = BLOCK / 32;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    T inc = warp_inclusive_scan(v);
+    if (lane == 31) warp_tot[wid] = inc;
+    __syncthreads();
+    if (wid == 0) {
+        T t = lane < NW ? warp_tot[lane] : T(0);
+        T ti = warp_inclusive_scan(t);
+        if (lane < NW) warp_tot[lane] = ti - t;  // exclusive warp offsets
+        if (lane == NW - 1) *total = ti;
+    }
+    __syncthreads();
+    T r = warp_tot[wid] + inc - v;
+    return r;
+}
+
+// ---- decoupled look-back (single-pass chained scan over tiles) ----------------------------
+// Tile status word: [63:62] flag (0 empty, 1 aggregate, 2 inclusive prefix), [61:0] value.
+constexpr uint64_t LB_VALUE_MASK = (uint64_t(1) << 62) - 1;
+__device__ __forceinline__ uint64_t lb_pack(uint64_t flag, uint64_t v) { return (flag << 62) | v; }
+
+// Called by all threads of the block after the block aggregate is known.  Returns the
+// exclusive prefix of tile `tile` (sum of the aggregates of all earlier tiles).  Tiles must
+// be numbered in launch order via a ticket (fa::next_tile) so every predecessor is resident
+// or finished, which guarantees forward progress.
+__device__ __forceinline__ uint64_t lookback_prefix(uint64_t* status, int64_t tile, uint64_t aggregate,
+                                                     uint64_t* s_prefix) {
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        if (tile == 0) {
+            if (lane == 0) {
+                st_volatile_u64(&status[0], lb_pack(2, aggregate));
+                *s_prefix = 0;
+            }
+        } else {
+            if (lane == 0) st_volatile_u64(&status[tile], lb_pack(1, aggregate));
+            uint64_t excl = 0;
+            int64_t pred = tile - 1;
+            while (true) {
+                int64_t t = pred - lane;
+                uint64_t w = t >= 0 ? ld_volatile_u64(&status[t]) : lb_pack(2, 0);
+                uint64_t flag = w >> 62;
+                if (__any_sync(0xffffffffu, flag == 0)) {
+                    __nanosleep(32);
+                    continue;
+                }
+                unsigned pmask = __ballot_sync(0xffffffffu, flag == 2);
+                int first = pmask ? __ffs(pmask) - 1 : 32;
+                uint64_t val = lane <= first ? (w & LB_VALUE_MASK) : 0;
+                excl += warp_sum(val);
+                if (pmask) break;
+                pred -= 32;
+            }
+            if (lane == 0) {
+                st_volatile_u64(&status[tile], lb_pack(2, excl + aggregate));
+                *s_prefix = excl;
+            }
+        }
+    }
+    __syncthreads();
+    return *s_prefix;
+}
+
+__device__ __forceinline__ int64_t next_tile(unsigned long long* ticket, int64_t* s_tile) {
+    if (threadIdx.x == 0) *s_tile = static_cast<int64_t>(atomicAdd(ticket, 1ull));
+    __syncthreads();
+    return *s_tile;
+}
+
+}  // namespace fa

@@ -1,0 +1,134 @@
+// Bit-exact P1 element values of the reference OptV2 batch kernels.
+//
+// numpy evaluates every expression left to right and rounds after each operation; the
+// functions below repeat the reference's operation order with explicit round-to-nearest
+// intrinsics (__dmul_rn/__dadd_rn/__dsub_rn/__ddiv_rn), so no FMA contraction can change a
+// bit whatever the compiler flags, and divisions stay true divisions (never a reciprocal
+// multiply).  Sources:
+//   areas     mesh.py:62-65          0.5*|(x2-x1)(y3-y1) - (x3-x1)(y2-y1)|
+//   mass      assembly.py:219-224    diag area/6.0, off-diagonal area/12.0
+//   massw     assembly.py:232-242    W_b = (tw_b*area)/30.0 and the six row formulas
+//   stiff     assembly.py:251-263    dot(e_a, e_b)/(4.0*area), edges u=q2-q3, v=q3-q1, w=q1-q2
+//   gradients assembly.py:203-210    g_b = (e_b.y*inv2a, (-e_b.x)*inv2a), inv2a = 0.5/area
+//   elastic   assembly.py:278-306    21 lower-triangle rows, upper = copies
+// Entry (a, b) of an element matrix with a < b is the stored copy of (b, a) (the reference
+// computes the lower triangle and copies it, assembly.py:242, :263, :304-306).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "fa_common.cuh"
+
+namespace fa {
+
+#define FMUL __dmul_rn
+#define FADD __dadd_rn
+#define FSUB __dsub_rn
+#define FDIV __ddiv_rn
+
+template <typename T>
+__device__ __forceinline__ T sel3(int i, T x0, T x1, T x2) {
+    return i == 0 ? x0 : (i == 1 ? x1 : x2);
+}
+
+// compute_areas (mesh.py:62-65) with corners in triangle order.
+__device__ __forceinline__ double tri_area(double2 p1, double2 p2, double2 p3) {
+    double cross = FSUB(FMUL(FSUB(p2.x, p1.x), FSUB(p3.y, p1.y)), FMUL(FSUB(p3.x, p1.x), FSUB(p2.y, p1.y)));
+    return FMUL(0.5, fabs(cross));
+}
+
+// ---- per-kind prepared triangle data ---------------------------------------------------
+
+struct MassTri {
+    double d, o;  // area/6.0, area/12.0
+};
+__device__ __forceinline__ MassTri mass_prepare(double area) {
+    return {FDIV(area, 6.0), FDIV(area, 12.0)};
+}
+__device__ __forceinline__ double mass_entry(const MassTri& t, int a, int b) { return a == b ? t.d : t.o; }
+
+struct MasswTri {
+    double e00, e10, e20, e11, e21, e22;  // lower-triangle entries (row il = a + 3b)
+};
+__device__ __forceinline__ MasswTri massw_prepare(double area, double tw0, double tw1, double tw2) {
+    const double W1 = FDIV(FMUL(tw0, area), 30.0);
+    const double W2 = FDIV(FMUL(tw1, area), 30.0);
+    const double W3 = FDIV(FMUL(tw2, area), 30.0);
+    MasswTri t;
+    t.e00 = FADD(FADD(FMUL(3.0, W1), W2), W3);     // kg[0] = 3*w1 + w2 + w3
+    t.e10 = FADD(FADD(W1, W2), FDIV(W3, 2.0));     // kg[1] = w1 + w2 + w3/2
+    t.e20 = FADD(FADD(W1, FDIV(W2, 2.0)), W3);     // kg[2] = w1 + w2/2 + w3
+    t.e11 = FADD(FADD(W1, FMUL(3.0, W2)), W3);     // kg[4] = w1 + 3*w2 + w3
+    t.e21 = FADD(FADD(FDIV(W1, 2.0), W2), W3);     // kg[5] = w1/2 + w2 + w3
+    t.e22 = FADD(FADD(W1, W2), FMUL(3.0, W3));     // kg[8] = w1 + w2 + 3*w3
+    return t;
+}
+__device__ __forceinline__ double massw_entry(const MasswTri& t, int a, int b) {
+    const int hi = a > b ? a : b, lo = a > b ? b : a;
+    // (hi, lo) in {(0,0),(1,0),(2,0),(1,1),(2,1),(2,2)}
+    if (lo == 0) return sel3(hi, t.e00, t.e10, t.e20);
+    if (lo == 1) return hi == 1 ? t.e11 : t.e21;
+    return t.e22;
+}
+
+struct StiffTri {
+    double2 e0, e1, e2;  // u = q2 - q3, v = q3 - q1, w = q1 - q2
+    double a4;           // 4.0 * area
+};
+__device__ __forceinline__ double2 dsub2(double2 a, double2 b) { return make_double2(FSUB(a.x, b.x), FSUB(a.y, b.y)); }
+__device__ __forceinline__ StiffTri stiff_prepare(double2 p1, double2 p2, double2 p3, double area) {
+    return {dsub2(p2, p3), dsub2(p3, p1), dsub2(p1, p2), FMUL(4.0, area)};
+}
+__device__ __forceinline__ double stiff_entry(const StiffTri& t, int a, int b) {
+    // kg row for (a, b) is (e_a * e_b).sum(axis=1) / a4.  numpy's sum over the length-2 axis
+    // starts from the additive identity, ((0.0 + x*x') + y*y'), which only matters for the
+    // sign of an exact zero.  IEEE products commute, so the stored lower entry equals the
+    // same formula evaluated for (a, b).
+    const double2 ea = sel3(a, t.e0, t.e1, t.e2);
+    const double2 eb = sel3(b, t.e0, t.e1, t.e2);
+    return FDIV(FADD(FADD(0.0, FMUL(ea.x, eb.x)), FMUL(ea.y, eb.y)), t.a4);
+}
+
+struct ElasticTri {
+    double2 g0, g1, g2;  // true basis gradients (g1, g2, g3 of the reference)
+    double area;
+};
+__device__ __forceinline__ ElasticTri elastic_prepare(double2 p1, double2 p2, double2 p3, double area) {
+    const double inv2a = FDIV(0.5, area);
+    const double2 u = dsub2(p2, p3), v = dsub2(p3, p1), w = dsub2(p1, p2);
+    ElasticTri t;
+    t.g0 = make_double2(FMUL(u.y, inv2a), FMUL(-u.x, inv2a));
+    t.g1 = make_double2(FMUL(v.y, inv2a), FMUL(-v.x, inv2a));
+    t.g2 = make_double2(FMUL(w.y, inv2a), FMUL(-w.x, inv2a));
+    t.area = area;
+    return t;
+}
+
+// Lower-triangle entry (i, j), i >= j, of the 6x6 element matrix in the interleaved order
+// (x1, y1, x2, y2, x3, y3).  With i = 2A+s, j = 2B+t (B <= A) every reference row
+// (assembly.py:283-303) has the form ((c1*gB.p)*gA.q + (c2*gB.r)*gA.s) * area where the
+// column vertex B's gradient always comes first:
+//   s=0,t=0: (P*gBx)*gAx + (M*gBy)*gAy          s=1,t=1: (P*gBy)*gAy + (M*gBx)*gAx
+//   s=1,t=0: (L*gBx)*gAy + (M*gBy)*gAx  (A>B)    (L*gBx)*gAy + (M*gBx)*gAy  (A==B)
+//   s=0,t=1: (L*gBy)*gAx + (M*gBx)*gAy  (A>B only)
+__device__ __forceinline__ double elastic_lower(const ElasticTri& T, int i, int j, double L, double M, double P) {
+    const int A = i >> 1, s = i & 1, B = j >> 1, t = j & 1;
+    const double2 gA = sel3(A, T.g0, T.g1, T.g2);
+    const double2 gB = sel3(B, T.g0, T.g1, T.g2);
+    double r;
+    if (s == 0 && t == 0) {
+        r = FADD(FMUL(FMUL(P, gB.x), gA.x), FMUL(FMUL(M, gB.y), gA.y));
+    } else if (s == 1 && t == 1) {
+        r = FADD(FMUL(FMUL(P, gB.y), gA.y), FMUL(FMUL(M, gB.x), gA.x));
+    } else if (s == 1) {  // t == 0
+        r = A == B ? FADD(FMUL(FMUL(L, gB.x), gA.y), FMUL(FMUL(M, gB.x), gA.y))
+                   : FADD(FMUL(FMUL(L, gB.x), gA.y), FMUL(FMUL(M, gB.y), gA.x));
+    } else {  // s == 0, t == 1, A > B
+        r = FADD(FMUL(FMUL(L, gB.y), gA.x), FMUL(FMUL(M, gB.x), gA.y));
+    }
+    return FMUL(r, T.area);
+}
+__device__ __forceinline__ double elastic_entry(const ElasticTri& T, int i, int j, double L, double M, double P) {
+    return i >= j ? elastic_lower(T, i, j, L, M, P) : elastic_lower(T, j, i, L, M, P);
+}
+}  // namespace fa

@@ -1,0 +1,156 @@
+"""Generate the golden fixtures by running the REAL reference package (femasm) in the build
+container, where /root/reference exists.  The GPU box never runs this script: it only reads
+the committed outputs.
+
+    python tests/golden/make_golden.py small           -> tests/golden/small_cases.npz
+    python tests/golden/make_golden.py digests C1 C2   -> tests/golden/reference_digests.json
+
+small_cases.npz: seeded BASELINE-family meshes (tiny N), the reference's own generators
+(square / disk) and the reference's OptV2 output for every kind, as full arrays.
+reference_digests.json: SHA-256 of the reference's CSC arrays for the BASELINE configs
+(seeds 0..2), so full-size parity on the GPU box is checked against the reference itself.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import json
+import sys
+import time
+from pathlib import Path
+
+import numpy as np
+
+HERE = Path(__file__).resolve().parent
+REPO = HERE.parents[1]
+sys.path.insert(0, str(REPO))
+sys.path.insert(0, "/root/reference/pkg/src")
+
+import femasm  # noqa: E402  (the reference, read-only)
+
+from paper_1305_3122_b200.meshgen import BASELINE_CONFIGS, seeded_square_mesh  # noqa: E402
+
+KIND = {
+    "mass": femasm.MatrixKind.MASS,
+    "massw": femasm.MatrixKind.WEIGHTED_MASS,
+    "stiff": femasm.MatrixKind.STIFFNESS,
+    "elastic": femasm.MatrixKind.ELASTIC,
+}
+
+
+def digest(*arrays) -> str:
+    h = hashlib.sha256()
+    for a in arrays:
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
+
+
+def mesh_digest(m) -> str:
+    return digest(m.vertices.astype("<f8"), m.connectivity.astype("<i8"), m.weights.astype("<f8"))
+
+
+def ref_assemble(V, C, kind, w=None, lam=1.0, mu=0.5):
+    mesh = femasm.Mesh(V, C)
+    kw = {}
+    if kind == "massw":
+        tw = np.asarray(w, dtype=np.float64)
+        kw["weight"] = femasm.WeightField("samples", lambda x, y: tw)
+    if kind == "elastic":
+        kw["params"] = femasm.ElasticParams(lam, mu)
+    m = femasm.assemble(mesh, KIND[kind], femasm.Strategy.OPTV2, **kw)
+    return mesh, m
+
+
+def small():
+    out = {}
+    cases = []
+    for n in (2, 5, 16):
+        for seed in (0, 1):
+            sm = seeded_square_mesh(n, seed)
+            name = f"seeded_n{n}_s{seed}"
+            out[f"{name}/V"] = sm.vertices
+            out[f"{name}/C"] = sm.connectivity
+            out[f"{name}/w"] = sm.weights
+            for kind in KIND:
+                lam, mu = (2.0, 0.7) if seed == 1 else (1.0, 0.5)
+                mesh, m = ref_assemble(sm.vertices, sm.connectivity, kind, sm.weights, lam, mu)
+                out[f"{name}/{kind}/col_ptr"] = m.col_ptr
+                out[f"{name}/{kind}/row_idx"] = m.row_idx
+                out[f"{name}/{kind}/values"] = m.values
+                out[f"{name}/{kind}/lam_mu"] = np.array([lam, mu])
+            out[f"{name}/areas"] = mesh.areas
+            # batch kernels of the reference on the same mesh
+            out[f"{name}/kg_stiff"] = femasm.batch_kg_stiff(mesh)
+            out[f"{name}/kg_elastic"] = femasm.batch_kg_elastic(mesh, femasm.ElasticParams(1.0, 0.5))
+            out[f"{name}/kg_massw"] = femasm.batch_kg_mass_weighted(
+                mesh, femasm.WeightField("samples", lambda x, y, w=sm.weights: w))
+            out[f"{name}/kg_mass"] = femasm.batch_kg_mass(mesh.areas)
+            g = femasm.batch_gradients(mesh)
+            out[f"{name}/grad"] = np.concatenate([g.g1, g.g2, g.g3])
+            cases.append(name)
+    # the reference's own structured generators, with its test defaults
+    gens = {
+        "square_n4": femasm.generate_unit_square_mesh(4),
+        "square_n1": femasm.generate_unit_square_mesh(1),
+        "disk_n4": femasm.generate_disk_mesh(4),
+        "disk_n6": femasm.generate_disk_mesh(6),
+    }
+    for name, mesh in gens.items():
+        out[f"{name}/V"] = mesh.vertices
+        out[f"{name}/C"] = mesh.connectivity
+        out[f"{name}/areas"] = mesh.areas
+        for kind in KIND:
+            kw = {}
+            if kind == "massw":
+                kw["weight"] = femasm.WeightField.quadratic()
+            if kind == "elastic":
+                kw["params"] = femasm.ElasticParams(1.0, 1.0)
+            m = femasm.assemble(mesh, KIND[kind], femasm.Strategy.OPTV2, **kw)
+            out[f"{name}/{kind}/col_ptr"] = m.col_ptr
+            out[f"{name}/{kind}/row_idx"] = m.row_idx
+            out[f"{name}/{kind}/values"] = m.values
+    np.savez_compressed(HERE / "small_cases.npz", **out)
+    print("small cases:", cases + list(gens))
+
+
+def digests(names):
+    path = HERE / "reference_digests.json"
+    data = json.loads(path.read_text()) if path.exists() else {}
+    for spec in names:
+        # spec: C1 | C1:s1 | EL64 (elastic lam=2 mu=0.7 N=64 seed 0)
+        if spec.startswith("EL64"):
+            kind, n, lam, mu, seeds = "elastic", 64, 2.0, 0.7, [0]
+            cfg = "EL64"
+        else:
+            cfg, _, s = spec.partition(":")
+            kind, n, lam, mu = BASELINE_CONFIGS[cfg]
+            seeds = [int(s[1:])] if s else [0, 1, 2]
+            lam = 1.0 if lam is None else lam
+            mu = 0.5 if mu is None else mu
+        for seed in seeds:
+            t0 = time.perf_counter()
+            sm = seeded_square_mesh(n, seed)
+            mesh, m = ref_assemble(sm.vertices, sm.connectivity, kind, sm.weights, lam, mu)
+            t1 = time.perf_counter()
+            key = f"{cfg}/s{seed}"
+            data[key] = {
+                "kind": kind, "N": n, "seed": seed, "lam": lam, "mu": mu,
+                "nq": int(sm.nq), "nme": int(sm.nme), "nnz": int(m.nnz),
+                "mesh_sha256": mesh_digest(sm),
+                "areas_sha256": digest(mesh.areas.astype("<f8")),
+                "col_ptr_sha256": digest(m.col_ptr.astype("<i8")),
+                "row_idx_sha256": digest(m.row_idx.astype("<i8")),
+                "values_sha256": digest(m.values.astype("<f8")),
+                "values_sum": float(m.values.sum()),
+                "reference_seconds": round(t1 - t0, 2),
+            }
+            print(key, data[key]["nnz"], f"{t1 - t0:.1f}s", flush=True)
+            path.write_text(json.dumps(data, indent=1, sort_keys=True))
+            del mesh, m, sm
+
+
+if __name__ == "__main__":
+    if sys.argv[1] == "small":
+        small()
+    elif sys.argv[1] == "digests":
+        digests(sys.argv[2:])

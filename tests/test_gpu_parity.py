@@ -1,0 +1,163 @@
+"""GPU parity of the fused OptV2 path (fa_plan_build + fa_assemble via the C ABI) against
+the reference: golden full arrays (small meshes), reference digests (BASELINE sizes), the
+C oracle (row blocks, edge cases)."""
+
+import numpy as np
+import pytest
+
+import paper_1305_3122_b200 as fa
+from helpers import assert_same_csc, csc_digests
+from oracle import c_oracle
+from oracle import femasm_oracle as fo
+from paper_1305_3122_b200.meshgen import seeded_square_mesh
+
+pytestmark = pytest.mark.gpu
+
+KINDS = ("mass", "massw", "stiff", "elastic")
+SMALL = [f"seeded_n{n}_s{s}" for n in (2, 5, 16) for s in (0, 1)] + ["square_n4", "square_n1", "disk_n4", "disk_n6"]
+
+
+def plan_assemble(kind, V, C, areas, w=None, lam=1.0, mu=0.5, v0=0, v1=None, recompute=False):
+    import torch
+
+    nq, nme = V.shape[0], C.shape[0]
+    dev = torch.device("cuda")
+    me = torch.from_numpy(np.ascontiguousarray(C, dtype=np.int32)).to(dev)
+    q = torch.from_numpy(np.ascontiguousarray(V)).to(dev)
+    a = None if recompute else torch.from_numpy(np.ascontiguousarray(areas)).to(dev)
+    wd = torch.from_numpy(np.ascontiguousarray(w)).to(dev) if w is not None else None
+    plan = fa.AssemblyPlan(nme, nq, v0, nq if v1 is None else v1)
+    plan.build(me)
+    plan.check_build()
+    rowptr, col, val, r = plan.assemble(kind, q=q, areas=a, w=wd, lam=lam, mu=mu)
+    return (rowptr.cpu().numpy(), col.cpu().numpy(), val.cpu().numpy()), r
+
+
+def _case(golden, name, kind):
+    V, C = golden[f"{name}/V"], golden[f"{name}/C"]
+    w = golden.get(f"{name}/w")
+    if w is None:
+        w = 1.0 + V[:, 0] * V[:, 0] + V[:, 1] * V[:, 1]
+    lm = golden.get(f"{name}/{kind}/lam_mu")
+    lam, mu = (float(lm[0]), float(lm[1])) if lm is not None else (1.0, 1.0)
+    return V, C, golden[f"{name}/areas"], w, lam, mu
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("name", SMALL)
+def test_small_meshes_bitwise(golden, name, kind):
+    V, C, areas, w, lam, mu = _case(golden, name, kind)
+    got, r = plan_assemble(kind, V, C, areas, w, lam, mu)
+    ref = tuple(golden[f"{name}/{kind}/{f}"] for f in ("col_ptr", "row_idx", "values"))
+    assert_same_csc(got, ref, f"{name}/{kind}")
+    assert r.nnz == len(ref[2])
+
+
+@pytest.mark.parametrize("kind", ("stiff", "elastic", "mass"))
+def test_recomputed_areas_are_bitwise(golden, kind):
+    V, C, areas, w, lam, mu = _case(golden, "seeded_n16_s1", kind)
+    a, _ = plan_assemble(kind, V, C, areas, w, lam, mu)
+    b, _ = plan_assemble(kind, V, C, areas, w, lam, mu, recompute=True)
+    assert_same_csc(a, b, kind)
+
+
+@pytest.mark.parametrize("key", ["C1/s0", "C1/s1", "C1/s2", "EL64/s0", "C2/s0", "C2/s1", "C2/s2"])
+def test_reference_digests(digests, key):
+    if key not in digests:
+        pytest.skip("digest not generated")
+    d = digests[key]
+    sm = seeded_square_mesh(d["N"], d["seed"])
+    areas = c_oracle.areas(sm.vertices, sm.connectivity)
+    got, r = plan_assemble(d["kind"], sm.vertices, sm.connectivity, areas, sm.weights, d["lam"], d["mu"])
+    assert r.nnz == d["nnz"]
+    assert csc_digests(*got) == (d["col_ptr_sha256"], d["row_idx_sha256"], d["values_sha256"])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("key", ["C3/s0", "C4/s0", "C3/s1", "C4/s1"])
+def test_reference_digests_large(digests, key):
+    test_reference_digests(digests, key)
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("blocks", (2, 3, 8))
+def test_row_blocks_match_subset_oracle(kind, blocks):
+    sm = seeded_square_mesh(24, 3)
+    areas = c_oracle.areas(sm.vertices, sm.connectivity)
+    full = c_oracle.assemble(kind, sm.vertices, sm.connectivity, areas, sm.weights, 1.0, 0.5)
+    rpv = 2 if kind == "elastic" else 1
+    cuts = np.linspace(0, sm.nq, blocks + 1).astype(int)
+    for v0, v1 in zip(cuts[:-1], cuts[1:]):
+        got, _ = plan_assemble(kind, sm.vertices, sm.connectivity, areas, sm.weights, 1.0, 0.5, v0, v1)
+        lo, hi = full[0][rpv * v0], full[0][rpv * v1]
+        ref = (full[0][rpv * v0: rpv * v1 + 1] - lo, full[1][lo:hi], full[2][lo:hi])
+        assert_same_csc(got, ref, f"{kind} [{v0},{v1})")
+
+
+def fan_mesh(n_spokes, n_rings=2):
+    """Star around one hub vertex: degree n_spokes (> 8) exercises the general path."""
+    ang = 2 * np.pi * np.arange(n_spokes) / n_spokes
+    pts = [np.zeros((1, 2))]
+    for r in range(1, n_rings + 1):
+        pts.append(np.stack([r * np.cos(ang + 0.1 * r), r * np.sin(ang + 0.1 * r)], axis=1))
+    V = np.concatenate(pts)
+    tris = []
+    for j in range(n_spokes):
+        jn = (j + 1) % n_spokes
+        tris.append((0, 1 + j, 1 + jn))
+        for r in range(1, n_rings):
+            a, b = 1 + (r - 1) * n_spokes, 1 + r * n_spokes
+            tris.append((a + j, b + j, b + jn))
+            tris.append((a + j, b + jn, a + jn))
+    C = np.array(tris, dtype=np.int64)
+    rng = np.random.default_rng(n_spokes)
+    return V, C[rng.permutation(len(C))]
+
+
+@pytest.mark.parametrize("kind", KINDS)
+@pytest.mark.parametrize("spokes", (9, 17, 64))
+def test_high_degree_vertices_take_the_general_path(kind, spokes):
+    V, C = fan_mesh(spokes)
+    areas = fo.triangle_areas(V, C)
+    w = np.linspace(0.5, 2.0, V.shape[0])
+    ref = fo.assemble_optv2(kind, V, C, areas, w, 2.0, 0.7)
+    got, r = plan_assemble(kind, V, C, areas, w, 2.0, 0.7)
+    assert r.heavy_rows > 0
+    assert_same_csc(got, ref, f"fan{spokes}/{kind}")
+
+
+def test_deterministic_across_runs():
+    sm = seeded_square_mesh(64, 5)
+    areas = c_oracle.areas(sm.vertices, sm.connectivity)
+    a, _ = plan_assemble("elastic", sm.vertices, sm.connectivity, areas, None, 2.0, 0.7)
+    b, _ = plan_assemble("elastic", sm.vertices, sm.connectivity, areas, None, 2.0, 0.7)
+    assert_same_csc(a, b, "rerun")
+
+
+def test_zero_weight_gives_empty_matrix():
+    sm = seeded_square_mesh(6, 0)
+    areas = fo.triangle_areas(sm.vertices, sm.connectivity)
+    got, r = plan_assemble("massw", sm.vertices, sm.connectivity, areas, np.zeros(sm.nq))
+    assert r.nnz == 0 and not got[0].any()
+
+
+def test_degenerate_triangle_reports_first_index():
+    V = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0], [2.0, 0.0]])
+    C = np.array([[0, 1, 2], [0, 1, 3], [1, 3, 2], [0, 3, 1]])
+    areas = fo.triangle_areas(V, C)  # triangles 1 and 3 are collinear
+    for kind in ("mass", "stiff", "elastic"):
+        _, r = plan_assemble(kind, V, C, areas, None, 1.0, 1.0)
+        assert r.degenerate_index == 1, kind
+    _, r = plan_assemble("massw", V, C, areas, np.ones(4))
+    assert r.degenerate_index == fa._lib.INT64_MAX  # weighted mass never checks (assembly.py:227-243)
+
+
+def test_connectivity_out_of_range_is_reported():
+    import torch
+
+    V = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0]])
+    C = np.array([[0, 1, 2], [0, 1, 7]], dtype=np.int32)
+    plan = fa.AssemblyPlan(2, 3)
+    plan.build(torch.from_numpy(C).cuda())
+    with pytest.raises(ValueError, match="out of range"):
+        plan.check_build()
