@@ -152,6 +152,14 @@ int fa_triplets_to_csc(const int64_t* d_rows, const int64_t* d_cols, const doubl
                        int64_t* d_rowidx, double* d_vals_out, void* d_workspace,
                        size_t workspace_bytes, fa_result* d_result, void* stream);
 
+/* ------------------------------------------------------------------------------------
+ * Diagnostics.  fa_selftest_division compares the library's call-free correctly rounded
+ * fp64 division (used by every element value) bitwise with CUDA's __ddiv_rn on n generated
+ * operand pairs; *d_bad receives the mismatch count, d_first[0..3] = x, y, mine, ref of one.
+ * ---------------------------------------------------------------------------------- */
+int fa_selftest_division(int64_t n, uint64_t seed, unsigned long long* d_bad, double* d_first,
+                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -45,6 +45,7 @@ EXPORTED_SYMBOLS = (
     "fa_compute_areas",
     "fa_triplets_workspace",
     "fa_triplets_to_csc",
+    "fa_selftest_division",
 )
 
 
@@ -85,6 +86,7 @@ _SIGNATURES = {
     "fa_compute_areas": (_I, [_P, _I64, _P, _P, _P, _P]),
     "fa_triplets_workspace": (ctypes.c_size_t, [_I64, _I64, _I64]),
     "fa_triplets_to_csc": (_I, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, ctypes.c_size_t, _P, _P]),
+    "fa_selftest_division": (_I, [_I64, ctypes.c_uint64, _P, _P, _P]),
 }
 
 _lib = None

@@ -2,9 +2,9 @@
 //
 // numpy evaluates every expression left to right and rounds after each operation; the
 // functions below repeat the reference's operation order with explicit round-to-nearest
-// intrinsics (__dmul_rn/__dadd_rn/__dsub_rn/__ddiv_rn), so no FMA contraction can change a
-// bit whatever the compiler flags, and divisions stay true divisions (never a reciprocal
-// multiply).  Sources:
+// intrinsics (__dmul_rn/__dadd_rn/__dsub_rn and the correctly rounded fa::ddiv), so no FMA
+// contraction can change a bit whatever the compiler flags, and divisions stay true
+// divisions (never a reciprocal multiply).  Sources:
 //   areas     mesh.py:62-65          0.5*|(x2-x1)(y3-y1) - (x3-x1)(y2-y1)|
 //   mass      assembly.py:219-224    diag area/6.0, off-diagonal area/12.0
 //   massw     assembly.py:232-242    W_b = (tw_b*area)/30.0 and the six row formulas
@@ -18,13 +18,14 @@
 #include <cuda_runtime.h>
 
 #include "fa_common.cuh"
+#include "fa_div.cuh"
 
 namespace fa {
 
 #define FMUL __dmul_rn
 #define FADD __dadd_rn
 #define FSUB __dsub_rn
-#define FDIV __ddiv_rn
+#define FDIV ::fa::ddiv  // call-free correctly rounded division (fa_div.cuh)
 
 template <typename T>
 __device__ __forceinline__ T sel3(int i, T x0, T x1, T x2) {
@@ -56,10 +57,11 @@ __device__ __forceinline__ MasswTri massw_prepare(double area, double tw0, doubl
     const double W3 = FDIV(FMUL(tw2, area), 30.0);
     MasswTri t;
     t.e00 = FADD(FADD(FMUL(3.0, W1), W2), W3);     // kg[0] = 3*w1 + w2 + w3
-    t.e10 = FADD(FADD(W1, W2), FDIV(W3, 2.0));     // kg[1] = w1 + w2 + w3/2
-    t.e20 = FADD(FADD(W1, FDIV(W2, 2.0)), W3);     // kg[2] = w1 + w2/2 + w3
+    // x / 2.0 == x * 0.5 exactly (division by a power of two is an exact rescale in both)
+    t.e10 = FADD(FADD(W1, W2), FMUL(W3, 0.5));     // kg[1] = w1 + w2 + w3/2
+    t.e20 = FADD(FADD(W1, FMUL(W2, 0.5)), W3);     // kg[2] = w1 + w2/2 + w3
     t.e11 = FADD(FADD(W1, FMUL(3.0, W2)), W3);     // kg[4] = w1 + 3*w2 + w3
-    t.e21 = FADD(FADD(FDIV(W1, 2.0), W2), W3);     // kg[5] = w1/2 + w2 + w3
+    t.e21 = FADD(FADD(FMUL(W1, 0.5), W2), W3);     // kg[5] = w1/2 + w2 + w3
     t.e22 = FADD(FADD(W1, W2), FMUL(3.0, W3));     // kg[8] = w1 + w2 + 3*w3
     return t;
 }

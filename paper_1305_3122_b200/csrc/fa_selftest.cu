@@ -1,0 +1,55 @@
+// Device self-tests exported through the C ABI (diagnostics, not on the assembly path).
+#include "fa_common.cuh"
+#include "fa_div.cuh"
+
+namespace fa {
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ull;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+    return x ^ (x >> 31);
+}
+
+// Operand generator mixing raw bit patterns (every exponent, subnormals, inf, nan, zeros),
+// values near 1 and the magnitudes the assembly divides (areas, weights, dot products).
+__device__ __forceinline__ double gen_operand(uint64_t h) {
+    const int mode = int(h & 7);
+    const uint64_t r = splitmix64(h);
+    switch (mode) {
+        case 0: return __longlong_as_double(r);                                   // any bits
+        case 1: return __longlong_as_double(r & 0x800fffffffffffffull);           // subnormal / zero
+        case 2: return 1.0 + double(r >> 11) * 0x1.0p-53;                         // [1, 2)
+        case 3: return __longlong_as_double((r & 0x800fffffffffffffull) | (uint64_t(1023 + int(r >> 52) % 40 - 20) << 52));
+        case 4: return double(int64_t(r % 2000001) - 1000000);                      // integers
+        case 5: return __longlong_as_double((r & 0x800fffffffffffffull) | (uint64_t(1 + (r >> 40) % 2046) << 52));
+        case 6: return double(r >> 11) * 0x1.0p-53 * 1e-6;                         // small areas
+        default: return __longlong_as_double(r & 0xfff0000000000000ull);          // powers of two / inf
+    }
+}
+
+__global__ void k_selftest_div(int64_t n, uint64_t seed, unsigned long long* bad, double* first) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+        const uint64_t h = splitmix64(seed ^ uint64_t(i) * 0x2545f4914f6cdd1dull);
+        const double x = gen_operand(h), y = gen_operand(splitmix64(h + 17));
+        const double mine = ddiv(x, y), ref = __ddiv_rn(x, y);
+        const bool both_nan = mine != mine && ref != ref;
+        if (!both_nan && __double_as_longlong(mine) != __double_as_longlong(ref)) {
+            if (atomicAdd(bad, 1ull) == 0) {
+                first[0] = x; first[1] = y; first[2] = mine; first[3] = ref;
+            }
+        }
+    }
+}
+
+}  // namespace fa
+
+extern "C" int fa_selftest_division(int64_t n, uint64_t seed, unsigned long long* d_bad, double* d_first,
+                                    void* stream) {
+    if (n < 0 || !d_bad || !d_first) { fa::set_error("fa_selftest_division: bad argument"); return FA_ERR_ARGUMENT; }
+    cudaStream_t st = fa::as_stream(stream);
+    FA_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(unsigned long long), st));
+    fa::k_selftest_div<<<fa::grid_for(n, 256), 256, 0, st>>>(n, seed, d_bad, d_first);
+    FA_LAUNCH_CHECK("k_selftest_div");
+    return FA_OK;
+}

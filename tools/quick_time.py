@@ -1,30 +1,28 @@
 """Quick device timing of plan build + numeric assembly per config (development tool)."""
-import sys, time
+import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import numpy as np
 import torch
 import paper_1305_3122_b200 as fa
+from paper_1305_3122_b200.device import ResultBlock
 from paper_1305_3122_b200.meshgen import seeded_square_mesh, BASELINE_CONFIGS
 
-def run(cfg, reps=10):
+def run(cfg, reps=10, recompute=True):
     kind, n, lam, mu = BASELINE_CONFIGS[cfg]
     sm = seeded_square_mesh(n, 0)
     dev = torch.device("cuda")
     me = torch.from_numpy(sm.connectivity.astype(np.int32)).to(dev)
     q = torch.from_numpy(sm.vertices).to(dev)
     areas = fa.compute_areas(sm.vertices, sm.connectivity)
-    a = torch.from_numpy(areas).to(dev)
+    a = None if (recompute and kind in ("stiff", "elastic")) else torch.from_numpy(areas).to(dev)
     w = torch.from_numpy(sm.weights).to(dev) if kind == "massw" else None
     plan = fa.AssemblyPlan(sm.nme, sm.nq)
     plan.build(me); plan.check_build()
     cap = plan.capacity(kind)
-    rows = plan.rows(kind)
-    rowptr = torch.empty(rows + 1, dtype=torch.int64, device=dev)
+    rowptr = torch.empty(plan.rows(kind) + 1, dtype=torch.int64, device=dev)
     col = torch.empty(cap, dtype=torch.int32, device=dev)
     val = torch.empty(cap, dtype=torch.float64, device=dev)
-    res = fa.device.ResultBlock() if hasattr(fa, "device") else None
-    from paper_1305_3122_b200.device import ResultBlock
     res = ResultBlock()
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
     e = [torch.cuda.Event(enable_timing=True) for _ in range(3)]
