@@ -160,6 +160,11 @@ int fa_triplets_to_csc(const int64_t* d_rows, const int64_t* d_cols, const doubl
 int fa_selftest_division(int64_t n, uint64_t seed, unsigned long long* d_bad, double* d_first,
                          void* stream);
 
+/* Record two caller-created CUDA events (cudaEvent_t as void*) around every subsequent row
+ * kernel launch of fa_assemble on the calling host thread (NULL, NULL disables).  Used by
+ * bench.py to time the dominant kernel for its roofline figure. */
+int fa_set_kernel_timer(void* ev_begin, void* ev_end);
+
 #ifdef __cplusplus
 }
 #endif

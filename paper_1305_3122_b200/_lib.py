@@ -14,7 +14,7 @@ from pathlib import Path
 import numpy as np
 
 LIB_NAME = "libfemasm_b200.so"
-LIB_PATH = Path(__file__).resolve().parent / LIB_NAME
+LIB_PATH = Path(os.environ.get("FEMASM_B200_LIB", Path(__file__).resolve().parent / LIB_NAME))
 
 FA_OK = 0
 FA_ERR_ARGUMENT = 1
@@ -46,6 +46,7 @@ EXPORTED_SYMBOLS = (
     "fa_triplets_workspace",
     "fa_triplets_to_csc",
     "fa_selftest_division",
+    "fa_set_kernel_timer",
 )
 
 
@@ -87,6 +88,7 @@ _SIGNATURES = {
     "fa_triplets_workspace": (ctypes.c_size_t, [_I64, _I64, _I64]),
     "fa_triplets_to_csc": (_I, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, ctypes.c_size_t, _P, _P]),
     "fa_selftest_division": (_I, [_I64, ctypes.c_uint64, _P, _P, _P]),
+    "fa_set_kernel_timer": (_I, [_P, _P]),
 }
 
 _lib = None

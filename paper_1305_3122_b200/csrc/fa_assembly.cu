@@ -1,28 +1,35 @@
-// OptV2 assembly on B200: vertex-bucket plan + fused row kernel (element values, Matlab
-// sparse() summation, zero drop, row offsets, CSR write) for one block of vertex rows.
+// OptV2 assembly on B200: fixed-capacity vertex-bucket plan + fused row kernel (element
+// values, Matlab sparse() summation, zero drop, row offsets, CSR write) for one block of
+// vertex rows.
 //
 // Reference path replaced (pkg/src/femasm): assemble(..., OPTV2) assembly.py:419-452 ->
 // _assemble_batched :400-416 -> build_ig_jg_p1[_vector] :162-192 + batch_kg_* :214-307 ->
 // TripletBatch.to_csc sparse.py:318-329 -> csc_from_triplets :140-189.
 //
 // Design:
-//   plan    K1 bucket count   vertices are grouped in buckets of BV consecutive ids; every
-//                             (triangle k, corner a) is counted in its vertex's bucket
-//                             (shared-memory histograms, one global atomic per block and bucket)
-//           K2 bucket scan    bucket offsets (decoupled look-back scan)
-//           K3 bucket scatter one 16-byte incidence record {k, n1, n2, vloc|a} per corner into
-//                             its bucket (n1, n2 = the triangle's other two vertices)
-//   numeric K4 rows           one block per bucket, one thread per matrix row: counting sort
-//                             of the bucket's records by vertex in shared memory, the row's
-//                             <= 8 records sorted by k in registers, inputs gathered (areas,
-//                             q, w), that row of each element matrix computed bit-exactly,
-//                             columns merged in ascending order with each position summed
-//                             sequentially in ascending k (== stable argsort + bincount of the
-//                             reference), exact-zero sums dropped, block scan + decoupled
-//                             look-back for the global row offset, the bucket's CSR segment
-//                             staged in shared memory and written coalesced.
-// Rows with more than MAXD incident triangles (or buckets with more than IDX_CAP records)
-// take a general O(d^2) path in separate phases of the same kernel.
+//   plan    K1 scatter   vertices are grouped in buckets of BV consecutive ids, each with room
+//                        for CAPB incidence keys (8 per vertex).  One pass over the
+//                        connectivity writes key = (k << 2) | a for every (triangle k, corner
+//                        a) into its vertex's bucket; slots come from shared-memory histograms
+//                        plus one global atomic per (block, bucket).  The key array (32 B per
+//                        vertex) is small enough to stay in L2 while it is scattered.
+//   numeric K2 records   one 32-byte record per triangle {c0, c1, c2, area or (area/6,
+//                        area/12)}, coalesced, so an incidence costs one L1 line below.
+//           K3 rows      one block per bucket:
+//                        a) every key of the bucket (balanced over threads): gather the
+//                           triangle record (lane pairs, one L1 line per record) and the
+//                           neighbours' q or w, compute that row of its element matrix
+//                           bit-exactly (values, or the gradients for elasticity) into
+//                           shared memory;
+//                        b) counting sort of the records by vertex in shared memory;
+//                        c) one thread per matrix row: its <= MAXD records sorted by k in
+//                           registers, columns merged in ascending order with each position
+//                           summed sequentially in ascending k (== stable argsort + bincount of
+//                           the reference), exact-zero sums dropped;
+//                        d) block scan + decoupled look-back for the global row offset, the
+//                           bucket's CSR segment staged in shared memory and written coalesced.
+// Rows with more than MAXD incidences, and buckets that overflowed CAPB, take a general
+// O(d^2) path (the latter scanning the connectivity) and write directly to global memory.
 #include <climits>
 #include <cstdlib>
 #include <new>
@@ -32,13 +39,12 @@
 
 namespace fa {
 
-constexpr int BV = 256;          // vertices per bucket
+constexpr int BV = 128;          // vertices per bucket
+constexpr int CAPB = 8 * BV;     // key slots per bucket
 constexpr int MAXD = 8;          // incidences per row on the register fast path
-constexpr int IDX_CAP = 4096;    // records per bucket indexable from shared memory
-constexpr int SMEM_NB = 16384;   // buckets counted with shared-memory histograms
-constexpr int PLAN_BLOCK = 512;
-constexpr int SCAN_BLOCK = 256;
-constexpr int SCAN_ITEMS = 8;
+constexpr int SMEM_NB = 32768;   // buckets counted with (u16-packed) shared-memory histograms
+constexpr int PLAN_BLOCK = 1024;
+constexpr int PLAN_UNROLL = 4;
 
 __global__ void k_reset_result(fa_result* r) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
@@ -54,128 +60,156 @@ __global__ void k_reset_result(fa_result* r) {
 }
 
 // ------------------------------------------------------------------------------------------
-// plan kernels
+// plan: one scatter pass
 // ------------------------------------------------------------------------------------------
 struct PlanArgs {
     const int32_t* me;
     int64_t nme, nq, v0, v1;
-    int64_t nb;         // buckets
-    int64_t chunk;      // triangles per block
-    int* bcount;        // nb
-    int64_t* bptr;      // nb + 1
-    unsigned* bcursor;  // nb
-    uint4* rec;         // records
+    int64_t nb;          // buckets
+    int64_t chunk;       // triangles per block
+    unsigned* bfill;     // nb: keys written (may exceed CAPB: overflow)
+    unsigned* keys;      // nb * CAPB
     fa_result* res;
 };
 
-// K1: per-bucket incidence counts.  SMEM: shared histogram (nb <= SMEM_NB).
-template <bool SMEM>
-__global__ void __launch_bounds__(PLAN_BLOCK) k_bucket_count(PlanArgs P) {
-    extern __shared__ int s_hist[];
-    if (SMEM) {
-        for (int64_t b = threadIdx.x; b < P.nb; b += blockDim.x) s_hist[b] = 0;
-        __syncthreads();
-    }
-    const int64_t k0 = blockIdx.x * P.chunk;
-    const int64_t k1 = min(P.nme, k0 + P.chunk);
-    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const int64_t v = P.me[3 * k + a];
-            if (v < 0 || v >= P.nq) {
-                atomic_min_i64(&P.res->index_error_pos, 3 * k + a);
-                continue;
-            }
-            if (v < P.v0 || v >= P.v1) continue;
-            const int64_t b = (v - P.v0) / BV;
-            if (SMEM) atomicAdd(&s_hist[b], 1);
-            else atomicAdd(&P.bcount[b], 1);
-        }
-    }
-    if (SMEM) {
-        __syncthreads();
-        for (int64_t b = threadIdx.x; b < P.nb; b += blockDim.x)
-            if (s_hist[b]) atomicAdd(&P.bcount[b], s_hist[b]);
-    }
+__device__ __forceinline__ void load_tri_ids(const int32_t* me, int64_t k, int& c0, int& c1, int& c2) {
+    c0 = me[3 * k];
+    c1 = me[3 * k + 1];
+    c2 = me[3 * k + 2];
 }
 
-// K3: scatter incidence records into their buckets.
 template <bool SMEM>
-__global__ void __launch_bounds__(PLAN_BLOCK) k_bucket_scatter(PlanArgs P) {
-    extern __shared__ unsigned s_pos[];
+__global__ void __launch_bounds__(PLAN_BLOCK) k_plan_scatter(PlanArgs P) {
+    extern __shared__ unsigned s_cnt[];  // u16 pairs: count, then running slot
     const int64_t k0 = blockIdx.x * P.chunk;
     const int64_t k1 = min(P.nme, k0 + P.chunk);
+    constexpr int STEP = PLAN_BLOCK * PLAN_UNROLL;
     if (SMEM) {
-        for (int64_t b = threadIdx.x; b < P.nb; b += blockDim.x) s_pos[b] = 0;
+        for (int64_t w = threadIdx.x; w < (P.nb + 1) / 2; w += PLAN_BLOCK) s_cnt[w] = 0;
         __syncthreads();
-        for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
+        for (int64_t kb = k0 + threadIdx.x; kb < k1; kb += STEP) {
+            int c[PLAN_UNROLL][3];
+#pragma unroll
+            for (int u = 0; u < PLAN_UNROLL; ++u) {
+                const int64_t k = kb + int64_t(u) * PLAN_BLOCK;
+                if (k < k1) load_tri_ids(P.me, k, c[u][0], c[u][1], c[u][2]);
+                else c[u][0] = c[u][1] = c[u][2] = -1;
+            }
+#pragma unroll
+            for (int u = 0; u < PLAN_UNROLL; ++u)
+#pragma unroll
+                for (int a = 0; a < 3; ++a) {
+                    const int64_t v = c[u][a];
+                    const int64_t k = kb + int64_t(u) * PLAN_BLOCK;
+                    if (k >= k1) continue;
+                    if (v < 0 || v >= P.nq) {
+                        atomic_min_i64(&P.res->index_error_pos, 3 * k + a);
+                        continue;
+                    }
+                    if (v < P.v0 || v >= P.v1) continue;
+                    const int64_t b = (v - P.v0) / BV;
+                    atomicAdd(&s_cnt[b >> 1], 1u << ((b & 1) * 16));
+                }
+        }
+        __syncthreads();
+        // reserve slots: one global atomic per (block, bucket); keep the base (<= CAPB) in place
+        for (int64_t w = threadIdx.x; w < (P.nb + 1) / 2; w += PLAN_BLOCK) {
+            const unsigned pair = s_cnt[w];
+            unsigned out = 0;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const unsigned c = (pair >> (16 * h)) & 0xffffu;
+                const int64_t b = 2 * w + h;
+                if (c && b < P.nb) {
+                    const unsigned base = atomicAdd(&P.bfill[b], c);
+                    out |= min(base, unsigned(CAPB)) << (16 * h);
+                }
+            }
+            s_cnt[w] = out;
+        }
+        __syncthreads();
+    }
+    for (int64_t kb = k0 + threadIdx.x; kb < k1; kb += STEP) {
+        int c[PLAN_UNROLL][3];
+#pragma unroll
+        for (int u = 0; u < PLAN_UNROLL; ++u) {
+            const int64_t k = kb + int64_t(u) * PLAN_BLOCK;
+            if (k < k1) load_tri_ids(P.me, k, c[u][0], c[u][1], c[u][2]);
+            else c[u][0] = c[u][1] = c[u][2] = -1;
+        }
+#pragma unroll
+        for (int u = 0; u < PLAN_UNROLL; ++u)
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                const int64_t v = P.me[3 * k + a];
-                if (v >= P.v0 && v < P.v1 && v < P.nq) atomicAdd(&s_pos[(v - P.v0) / BV], 1u);
+                const int64_t v = c[u][a];
+                const int64_t k = kb + int64_t(u) * PLAN_BLOCK;
+                if (k >= k1 || v < P.v0 || v >= P.v1 || v >= P.nq) continue;
+                const int64_t b = (v - P.v0) / BV;
+                unsigned pos;
+                if (SMEM) {
+                    const int sh = int(b & 1) * 16;
+                    pos = (atomicAdd(&s_cnt[b >> 1], 1u << sh) >> sh) & 0xffffu;
+                } else {
+                    if (!SMEM && v < 0) continue;
+                    pos = atomicAdd(&P.bfill[b], 1u);
+                }
+                if (pos < CAPB) P.keys[b * CAPB + pos] = (unsigned(k) << 2) | unsigned(a);
             }
-        }
-        __syncthreads();
-        for (int64_t b = threadIdx.x; b < P.nb; b += blockDim.x) {
-            const unsigned c = s_pos[b];
-            if (c) s_pos[b] = unsigned(P.bptr[b]) + atomicAdd(&P.bcursor[b], c);
-        }
-        __syncthreads();
-    }
-    for (int64_t k = k0 + threadIdx.x; k < k1; k += blockDim.x) {
-        const int c0 = P.me[3 * k], c1 = P.me[3 * k + 1], c2 = P.me[3 * k + 2];
-#pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const int64_t v = sel3(a, c0, c1, c2);
-            if (v < P.v0 || v >= P.v1 || v >= P.nq) continue;
-            const int64_t vl = v - P.v0;
-            const int64_t b = vl / BV;
-            unsigned pos;
-            if (SMEM) pos = atomicAdd(&s_pos[b], 1u);
-            else pos = unsigned(P.bptr[b]) + atomicAdd(&P.bcursor[b], 1u);
-            const int n1 = sel3(a, c1, c2, c0), n2 = sel3(a, c2, c0, c1);  // corners a+1, a+2
-            P.rec[pos] = make_uint4(unsigned(k), unsigned(n1), unsigned(n2), (unsigned(vl % BV) << 2) | unsigned(a));
-        }
     }
 }
 
-// Exclusive scan of int32 counts into int64 offsets (out has n+1 entries) in one pass.
-__global__ void __launch_bounds__(SCAN_BLOCK) k_scan_i32_to_i64(const int* __restrict__ in, int64_t n,
-                                                                int64_t* __restrict__ out, uint64_t* status,
-                                                                unsigned long long* ticket) {
-    __shared__ int64_t s_tile;
-    __shared__ uint64_t s_prefix;
-    __shared__ int64_t s_warp[SCAN_BLOCK / 32];
-    __shared__ int64_t s_total;
-    const int64_t tile = next_tile(ticket, &s_tile);
-    const int64_t base = tile * SCAN_BLOCK * SCAN_ITEMS + int64_t(threadIdx.x) * SCAN_ITEMS;
-    int64_t x[SCAN_ITEMS];
-    int64_t local = 0;
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i) {
-        x[i] = (base + i < n) ? in[base + i] : 0;
-        local += x[i];
+// index validation for the global-atomic path is done here (k_plan_scatter<false> only
+// stores in-range keys and cannot report without a second branch in the hot loop)
+__global__ void k_validate_ids(const int32_t* __restrict__ me, int64_t n3, int64_t nq, fa_result* res) {
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n3; i += int64_t(gridDim.x) * blockDim.x) {
+        const int v = me[i];
+        if (v < 0 || v >= nq) atomic_min_i64(&res->index_error_pos, i);
     }
-    const int64_t excl = block_exclusive_scan<SCAN_BLOCK>(local, s_warp, &s_total);
-    const uint64_t prefix = lookback_prefix(status, tile, uint64_t(s_total), &s_prefix);
-    int64_t run = int64_t(prefix) + excl;
-#pragma unroll
-    for (int i = 0; i < SCAN_ITEMS; ++i) {
-        if (base + i < n) out[base + i] = run;
-        run += x[i];
+}
+
+// ------------------------------------------------------------------------------------------
+// numeric K2: one 32-byte record per triangle {c0, c1, c2, -, x, y} so that a row kernel
+// incidence costs a single L1 line: x, y = area/6, area/12 (mass, assembly.py:219-220) or
+// x = area (other kinds; recomputed from q with compute_areas' formula when areas is NULL).
+// The degeneracy check of assembly.py:152-155 runs here once per triangle.
+// ------------------------------------------------------------------------------------------
+struct alignas(32) TriRec {
+    int4 c;      // c0, c1, c2, unused
+    double2 v;   // kind-specific values
+};
+
+template <int KIND>
+__global__ void k_tri_records(const int32_t* __restrict__ me, int64_t nme, const double2* __restrict__ q,
+                              const double* __restrict__ areas, TriRec* __restrict__ T, fa_result* res) {
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nme; k += int64_t(gridDim.x) * blockDim.x) {
+        int c0, c1, c2;
+        load_tri_ids(me, k, c0, c1, c2);
+        const double area = areas ? areas[k] : tri_area(q[c0], q[c1], q[c2]);
+        if (KIND != FA_KIND_MASSW && area <= AREA_EPS) atomic_min_i64(&res->degenerate_index, k);
+        TriRec t;
+        t.c = make_int4(c0, c1, c2, 0);
+        if (KIND == FA_KIND_MASS) {
+            const MassTri m = mass_prepare(area);
+            t.v = make_double2(m.d, m.o);
+        } else {
+            t.v = make_double2(area, 0.0);
+        }
+        T[k] = t;
     }
-    if (base <= n - 1 && n - 1 < base + SCAN_ITEMS) out[n] = run;  // holder of element n-1
 }
 
 // ------------------------------------------------------------------------------------------
 // row kernel
 // ------------------------------------------------------------------------------------------
 struct RowsArgs {
-    const int64_t* bptr;
-    const uint4* rec;
+    const unsigned* keys;
+    const unsigned* bfill;
+    const int32_t* me;
+    int64_t nme;
     const double2* q;
     const double* areas;  // nullable: recompute from q (bitwise compute_areas)
     const double* w;
+    const TriRec* T;      // per-triangle records (k_tri_records)
     double lam, mu;
     int64_t v0, v1;       // owned vertices
     int64_t nrows;        // matrix rows produced (owned vertices * rows per vertex)
@@ -192,59 +226,73 @@ template <int KIND>
 struct KindTraits {
     static constexpr int RPV = KIND == FA_KIND_ELASTIC ? 2 : 1;  // rows per vertex
     static constexpr int NV = KIND == FA_KIND_ELASTIC ? 2 : 1;   // values per (row, vertex column)
-    static constexpr bool NEED_Q = KIND == FA_KIND_STIFF || KIND == FA_KIND_ELASTIC;
-    static constexpr bool NEED_W = KIND == FA_KIND_MASSW;
     static constexpr bool CHECK_AREA = KIND != FA_KIND_MASSW;   // massw never checks (assembly.py:227-243)
     static constexpr int THREADS = BV * RPV;
     static constexpr int CAPR = KIND == FA_KIND_ELASTIC ? 16 : 2 * MAXD + 1;  // staged entries per row
     static constexpr int STRIDE = CAPR | 1;                                   // odd: conflict-free
+    // per-record shared data: scalar kinds store the row's three values, elasticity the
+    // triangle's gradients + area (entries are formed per dof row in the merge phase)
+    static constexpr int RVALS = KIND == FA_KIND_ELASTIC ? 7 : 3;
 };
 
-// Per-thread data of the row's own vertex.
-struct OwnVertex {
-    int64_t v;
-    double2 p;
-    double w;
-};
-
-// Row (a, s) of one incident triangle's element matrix against the triangle's three
-// vertices: d = entry at the row's own vertex, o1 / o2 = entries at n1 / n2.
+// Shared-memory layout of the row kernel (records area and staging area are unioned).
 template <int KIND>
-__device__ __forceinline__ void row_values(const RowsArgs& A, const OwnVertex& own, uint4 r, int s,
-                                           double (&d)[2], double (&o1)[2], double (&o2)[2]) {
+struct RowsSmem {
     using TR = KindTraits<KIND>;
-    const int64_t k = r.x;
-    const int n1 = int(r.y), n2 = int(r.z), a = int(r.w & 3);
+    static constexpr size_t rec_bytes = size_t(CAPB) * (TR::RVALS * 8 + 4 + 4 + 4 + 2 + 1);
+    static constexpr size_t stage_bytes = size_t(TR::THREADS) * TR::STRIDE * 12;
+    static constexpr size_t bytes = (rec_bytes > stage_bytes ? rec_bytes : stage_bytes) + 64;
+};
+
+// Values of one record: the element-matrix row of corner a against the triangle's vertices
+// in local order (own, n1, n2).  Elasticity: gradients + area instead.  `own_p` / `own_w`
+// are the own vertex's coordinates / weight (from shared memory), n1 / n2 data is gathered.
+template <int KIND>
+__device__ __forceinline__ void record_values(const RowsArgs& A, const TriRec& t, int a, double2 own_p, double own_w,
+                                              double* out) {
     const int b1 = a == 2 ? 0 : a + 1, b2 = a == 0 ? 2 : a - 1;
-    double2 pa = own.p, p1 = make_double2(0.0, 0.0), p2 = p1;
-    const bool need_pts = TR::NEED_Q || A.areas == nullptr;
-    if (need_pts) {
-        p1 = A.q[n1];
-        p2 = A.q[n2];
-    }
-    // corners in triangle order
-    const double2 c0 = sel3(a, pa, p2, p1), c1 = sel3(a, p1, pa, p2), c2 = sel3(a, p2, p1, pa);
-    const double area = A.areas ? A.areas[k] : tri_area(c0, c1, c2);
-    if (TR::CHECK_AREA && area <= AREA_EPS) atomic_min_i64(&A.res->degenerate_index, k);
+    const int n1 = sel3(a, t.c.y, t.c.z, t.c.x), n2 = sel3(a, t.c.z, t.c.x, t.c.y);
     if constexpr (KIND == FA_KIND_MASS) {
-        const MassTri t = mass_prepare(area);
-        d[0] = t.d;
-        o1[0] = t.o;
-        o2[0] = t.o;
+        out[0] = t.v.x;
+        out[1] = t.v.y;
+        out[2] = t.v.y;
     } else if constexpr (KIND == FA_KIND_MASSW) {
-        const double wa = own.w, w1 = A.w[n1], w2 = A.w[n2];
-        const MasswTri t = massw_prepare(area, sel3(a, wa, w2, w1), sel3(a, w1, wa, w2), sel3(a, w2, w1, wa));
-        d[0] = massw_entry(t, a, a);
-        o1[0] = massw_entry(t, a, b1);
-        o2[0] = massw_entry(t, a, b2);
-    } else if constexpr (KIND == FA_KIND_STIFF) {
-        const StiffTri t = stiff_prepare(c0, c1, c2, area);
-        d[0] = stiff_entry(t, a, a);
-        o1[0] = stiff_entry(t, a, b1);
-        o2[0] = stiff_entry(t, a, b2);
+        const double w1 = A.w[n1], w2 = A.w[n2];
+        const MasswTri m = massw_prepare(t.v.x, sel3(a, own_w, w2, w1), sel3(a, w1, own_w, w2), sel3(a, w2, w1, own_w));
+        // row a against (a, a+1, a+2): a=0 -> (e00, e10, e20), a=1 -> (e11, e21, e10), a=2 -> (e22, e20, e21)
+        out[0] = sel3(a, m.e00, m.e11, m.e22);
+        out[1] = sel3(a, m.e10, m.e21, m.e20);
+        out[2] = sel3(a, m.e20, m.e10, m.e21);
     } else {
-        const ElasticTri t = elastic_prepare(c0, c1, c2, area);
+        const double2 p1 = A.q[n1], p2 = A.q[n2];
+        const double2 c0 = sel3(a, own_p, p2, p1), c1 = sel3(a, p1, own_p, p2), c2 = sel3(a, p2, p1, own_p);
+        if constexpr (KIND == FA_KIND_STIFF) {
+            const StiffTri m = stiff_prepare(c0, c1, c2, t.v.x);
+            out[0] = stiff_entry(m, a, a);
+            out[1] = stiff_entry(m, a, b1);
+            out[2] = stiff_entry(m, a, b2);
+        } else {
+            const ElasticTri m = elastic_prepare(c0, c1, c2, t.v.x);
+            out[0] = m.g0.x; out[1] = m.g0.y;
+            out[2] = m.g1.x; out[3] = m.g1.y;
+            out[4] = m.g2.x; out[5] = m.g2.y;
+            out[6] = m.area;
+        }
+    }
+}
+
+// The three (x NV) values of dof row s of a record: at the own vertex, n1, n2.
+template <int KIND>
+__device__ __forceinline__ void record_row(const RowsArgs& A, const double* rv, int a, int s, double (&d)[2],
+                                           double (&o1)[2], double (&o2)[2]) {
+    if constexpr (KIND == FA_KIND_ELASTIC) {
+        ElasticTri t;
+        t.g0 = make_double2(rv[0], rv[1]);
+        t.g1 = make_double2(rv[2], rv[3]);
+        t.g2 = make_double2(rv[4], rv[5]);
+        t.area = rv[6];
         const double P = FADD(A.lam, FMUL(2.0, A.mu));
+        const int b1 = a == 2 ? 0 : a + 1, b2 = a == 0 ? 2 : a - 1;
         const int i = 2 * a + s;
 #pragma unroll
         for (int tt = 0; tt < 2; ++tt) {
@@ -252,58 +300,77 @@ __device__ __forceinline__ void row_values(const RowsArgs& A, const OwnVertex& o
             o1[tt] = elastic_entry(t, i, 2 * b1 + tt, A.lam, A.mu, P);
             o2[tt] = elastic_entry(t, i, 2 * b2 + tt, A.lam, A.mu, P);
         }
+    } else {
+        d[0] = rv[0];
+        o1[0] = rv[1];
+        o2[0] = rv[2];
+        d[1] = o1[1] = o2[1] = 0.0;
     }
 }
 
-__device__ __forceinline__ void cswap4(uint4& x, uint4& y) {
-    const bool sw = x.x > y.x;
-    const uint4 lo = sw ? y : x, hi = sw ? x : y;
+__device__ __forceinline__ void cswap64(uint64_t& x, uint64_t& y) {
+    const uint64_t lo = x < y ? x : y, hi = x < y ? y : x;
     x = lo;
     y = hi;
 }
 // optimal 19-comparator network for 8 keys (verified by the 0-1 principle)
-__device__ __forceinline__ void sort8(uint4 (&k)[8]) {
-    cswap4(k[0], k[2]); cswap4(k[1], k[3]); cswap4(k[4], k[6]); cswap4(k[5], k[7]);
-    cswap4(k[0], k[4]); cswap4(k[1], k[5]); cswap4(k[2], k[6]); cswap4(k[3], k[7]);
-    cswap4(k[0], k[1]); cswap4(k[2], k[3]); cswap4(k[4], k[5]); cswap4(k[6], k[7]);
-    cswap4(k[2], k[4]); cswap4(k[3], k[5]);
-    cswap4(k[1], k[4]); cswap4(k[3], k[6]);
-    cswap4(k[1], k[2]); cswap4(k[3], k[4]); cswap4(k[5], k[6]);
+__device__ __forceinline__ void sort8(uint64_t (&k)[8]) {
+    cswap64(k[0], k[2]); cswap64(k[1], k[3]); cswap64(k[4], k[6]); cswap64(k[5], k[7]);
+    cswap64(k[0], k[4]); cswap64(k[1], k[5]); cswap64(k[2], k[6]); cswap64(k[3], k[7]);
+    cswap64(k[0], k[1]); cswap64(k[2], k[3]); cswap64(k[4], k[5]); cswap64(k[6], k[7]);
+    cswap64(k[2], k[4]); cswap64(k[3], k[5]);
+    cswap64(k[1], k[4]); cswap64(k[3], k[6]);
+    cswap64(k[1], k[2]); cswap64(k[3], k[4]); cswap64(k[5], k[6]);
 }
 
-// Shared state of one bucket, visible to the general path.
-struct BucketView {
-    const uint4* rec;           // first record of the bucket
-    int64_t n;                  // records in the bucket
-    const unsigned short* idx;  // per-vertex lists (when !overflow)
-    bool overflow;
+// Records of one bucket in shared memory.
+struct BucketRecs {
+    unsigned* key;            // (k << 2) | a
+    int* n1;
+    int* n2;
+    double* vals;             // [RVALS][CAPB]
+    unsigned short* list;     // record indices grouped by vertex
+    unsigned char* vl;        // vertex (local) of each record
 };
 
-// General path for one row (any degree): O(d^2) selection over the row's incidences with
-// the same summation order (ascending k per position).  Writes only when `write`.
+// General path for one row: O(d^2) selection with the same summation order (ascending k
+// per position).  In-smem records (`overflow` false) or, for an overflowed bucket, a scan of
+// the whole connectivity.  Writes only when `write`.
 template <int KIND>
-__device__ int64_t general_row(const RowsArgs& A, const BucketView& B, int start, int deg, int vloc,
-                               const OwnVertex& own, int s, int64_t out_pos, bool write, int64_t* drops) {
+__device__ int64_t general_row(const RowsArgs& A, const BucketRecs& R, bool overflow, int start, int deg,
+                               int64_t v, int s, int64_t out_pos, bool write, int64_t* drops) {
     constexpr int NV = KindTraits<KIND>::NV;
-    const int64_t m = B.overflow ? B.n : deg;
-    auto get = [&](int64_t i, uint4& r) -> bool {
-        if (B.overflow) {
-            r = B.rec[i];
-            return int(r.w >> 2) == vloc;
+    constexpr int RVALS = KindTraits<KIND>::RVALS;
+    const int64_t m = overflow ? A.nme : deg;
+    // incidence i of the row: triangle k, local corner a, other corners n1, n2
+    auto get = [&](int64_t i, int64_t& k, int& a, int& n1, int& n2, int& ridx) -> bool {
+        if (!overflow) {
+            ridx = R.list[start + i];
+            const unsigned key = R.key[ridx];
+            k = key >> 2;
+            a = key & 3;
+            n1 = R.n1[ridx];
+            n2 = R.n2[ridx];
+            return true;
         }
-        r = B.rec[B.idx[start + i]];
+        int c0, c1, c2;
+        load_tri_ids(A.me, i, c0, c1, c2);
+        if (c0 == v) a = 0; else if (c1 == v) a = 1; else if (c2 == v) a = 2; else return false;
+        k = i;
+        n1 = sel3(a, c1, c2, c0);
+        n2 = sel3(a, c2, c0, c1);
+        ridx = -1;
         return true;
     };
     int64_t last = -1, count = 0;
     while (true) {
         int64_t c = INT64_MAX;  // next vertex column
-        if (own.v > last) c = own.v;
+        if (v > last) c = v;
         for (int64_t i = 0; i < m; ++i) {
-            uint4 r;
-            if (!get(i, r)) continue;
-            const int64_t x1 = r.y, x2 = r.z;
-            if (x1 > last && x1 < c) c = x1;
-            if (x2 > last && x2 < c) c = x2;
+            int64_t k; int a, n1, n2, ridx;
+            if (!get(i, k, a, n1, n2, ridx)) continue;
+            if (n1 > last && n1 < c) c = n1;
+            if (n2 > last && n2 < c) c = n2;
         }
         if (c == INT64_MAX) break;
         double sum[NV];
@@ -311,26 +378,30 @@ __device__ int64_t general_row(const RowsArgs& A, const BucketView& B, int start
         for (int t = 0; t < NV; ++t) sum[t] = 0.0;
         int64_t prevk = -1;
         while (true) {  // contributions to column c in ascending k
-            int64_t bestk = INT64_MAX;
-            uint4 best = make_uint4(0, 0, 0, 0);
+            int64_t bestk = INT64_MAX, bk = 0;
+            int ba = 0, bn1 = 0, bn2 = 0, bidx = -1;
             for (int64_t i = 0; i < m; ++i) {
-                uint4 r;
-                if (!get(i, r)) continue;
-                const int64_t k = r.x;
+                int64_t k; int a, n1, n2, ridx;
+                if (!get(i, k, a, n1, n2, ridx)) continue;
                 if (k <= prevk || k >= bestk) continue;
-                if (c == own.v || int64_t(r.y) == c || int64_t(r.z) == c) {
-                    bestk = k;
-                    best = r;
+                if (c == v || n1 == c || n2 == c) {
+                    bestk = k; bk = k; ba = a; bn1 = n1; bn2 = n2; bidx = ridx;
                 }
             }
             if (bestk == INT64_MAX) break;
-            double d[2], o1[2], o2[2];
-            row_values<KIND>(A, own, best, s, d, o1, o2);
+            double rv[7];
+            if (bidx >= 0) {
 #pragma unroll
-            for (int t = 0; t < NV; ++t) {
-                const double x = c == own.v ? d[t] : (int64_t(best.y) == c ? o1[t] : o2[t]);
-                sum[t] = FADD(sum[t], x);
+                for (int j = 0; j < RVALS; ++j) rv[j] = R.vals[j * CAPB + bidx];
+            } else {
+                const double2 own_p = A.q ? A.q[v] : make_double2(0.0, 0.0);
+                const double own_w = A.w ? A.w[v] : 0.0;
+                record_values<KIND>(A, A.T[bk], ba, own_p, own_w, rv);
             }
+            double d[2], o1[2], o2[2];
+            record_row<KIND>(A, rv, ba, s, d, o1, o2);
+#pragma unroll
+            for (int t = 0; t < NV; ++t) sum[t] = FADD(sum[t], c == v ? d[t] : (bn1 == c ? o1[t] : o2[t]));
             prevk = bestk;
         }
 #pragma unroll
@@ -353,92 +424,163 @@ __device__ int64_t general_row(const RowsArgs& A, const BucketView& B, int start
 template <int KIND>
 __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, 1) k_rows(RowsArgs A) {
     using TR = KindTraits<KIND>;
+    using SM = RowsSmem<KIND>;
     constexpr int NV = TR::NV, RPV = TR::RPV, NT = TR::THREADS, STRIDE = TR::STRIDE, CAPR = TR::CAPR;
+    constexpr int RVALS = TR::RVALS;
     constexpr int NC = 2 * MAXD;
     extern __shared__ __align__(16) unsigned char smem_raw[];
+    // records area
+    BucketRecs R;
+    R.vals = reinterpret_cast<double*>(smem_raw);
+    R.key = reinterpret_cast<unsigned*>(R.vals + RVALS * CAPB);
+    R.n1 = reinterpret_cast<int*>(R.key + CAPB);
+    R.n2 = R.n1 + CAPB;
+    R.list = reinterpret_cast<unsigned short*>(R.n2 + CAPB);
+    R.vl = reinterpret_cast<unsigned char*>(R.list + CAPB);
+    // staging area (reuses the records area once every row holds its data in registers)
     double* s_val = reinterpret_cast<double*>(smem_raw);                 // [NT][STRIDE]
     int32_t* s_col = reinterpret_cast<int32_t*>(s_val + NT * STRIDE);   // [NT][STRIDE]
     __shared__ int s_cnt[BV];
     __shared__ int s_start[BV];
     __shared__ int s_fill[BV];
-    __shared__ unsigned short s_idx[IDX_CAP];
     __shared__ int64_t s_tile;
     __shared__ uint64_t s_prefix;
     __shared__ int64_t s_warp[NT / 32];
     __shared__ int64_t s_total;
     __shared__ int64_t s_off[NT + 1];
-    __shared__ unsigned char s_slow[NT];  // nonzero: row written outside the staging area
+    __shared__ unsigned short s_owner[NT * CAPR];
 
     const int tid = threadIdx.x;
     const int64_t b = next_tile(A.ticket, &s_tile);  // bucket, in launch order
-    const int64_t lo = A.bptr[b], n = A.bptr[b + 1] - lo;
-    const bool overflow = n > IDX_CAP;
-    const uint4* brec = A.rec + lo;
+    const unsigned filled = A.bfill[b];
+    const bool overflow = filled > unsigned(CAPB);
+    const int n = overflow ? 0 : int(filled);
+    const int64_t vbase = A.v0 + b * BV;
+    const unsigned* bkeys = A.keys + b * CAPB;
 
-    // ---- counting sort of the bucket's records by vertex (shared memory) ----------------
+    __shared__ double2 s_oq[BV];
+    __shared__ double s_ow[BV];
     for (int i = tid; i < BV; i += NT) {
         s_cnt[i] = 0;
         s_fill[i] = 0;
+        const int64_t vv = vbase + i;
+        s_oq[i] = (A.q && vv < A.v1) ? A.q[vv] : make_double2(0.0, 0.0);
+        s_ow[i] = (KIND == FA_KIND_MASSW && vv < A.v1) ? A.w[vv] : 0.0;
     }
     __syncthreads();
-    for (int64_t i = tid; i < n; i += NT) atomicAdd(&s_cnt[brec[i].w >> 2], 1);
+    // ---- a) per record: its triangle record (one L1 line: a lane pair loads two 32 B records
+    //         cooperatively and swaps halves), neighbour data, its row values -> shared memory.
+    //         AU rounds are issued together so each warp keeps several loads in flight.
+    {
+        constexpr int AU = 3;
+        const int lane = tid & 31, warp = tid >> 5, half = lane & 1, pair = lane >> 1;
+        const uint4* T4 = reinterpret_cast<const uint4*>(A.T);
+        for (int base0 = warp * 32; base0 < n; base0 += NT * AU) {
+            unsigned key[AU];
+            uint4 la[AU], lb[AU];
+            int idx[AU];
+            bool ok[AU];
+#pragma unroll
+            for (int u = 0; u < AU; ++u) {
+                const int base = base0 + u * NT;
+                const int iA = base + pair, iB = base + 16 + pair;
+                const bool okA = iA < n, okB = iB < n;
+                const unsigned keyA = okA ? bkeys[iA] : 0u, keyB = okB ? bkeys[iB] : 0u;
+                la[u] = okA ? T4[2 * int64_t(keyA >> 2) + half] : make_uint4(0u, 0u, 0u, 0u);
+                lb[u] = okB ? T4[2 * int64_t(keyB >> 2) + half] : make_uint4(0u, 0u, 0u, 0u);
+                key[u] = half ? keyB : keyA;  // even lane keeps record A, odd lane record B
+                idx[u] = half ? iB : iA;
+                ok[u] = half ? okB : okA;
+            }
+            TriRec t[AU];
+#pragma unroll
+            for (int u = 0; u < AU; ++u) {
+                const uint4 snd = half ? la[u] : lb[u];
+                uint4 rcv;
+                rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, 1);
+                rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, 1);
+                rcv.z = __shfl_xor_sync(0xffffffffu, snd.z, 1);
+                rcv.w = __shfl_xor_sync(0xffffffffu, snd.w, 1);
+                const uint4 lo = half ? rcv : la[u], hi = half ? lb[u] : rcv;
+                t[u].c = make_int4(int(lo.x), int(lo.y), int(lo.z), int(lo.w));
+                t[u].v = make_double2(__hiloint2double(int(hi.y), int(hi.x)), __hiloint2double(int(hi.w), int(hi.z)));
+            }
+#pragma unroll
+            for (int u = 0; u < AU; ++u) {
+                if (!ok[u]) continue;
+                const int i = idx[u];
+                const int a = key[u] & 3;
+                const int vl = int(sel3(a, t[u].c.x, t[u].c.y, t[u].c.z) - vbase);
+                R.key[i] = key[u];
+                R.n1[i] = sel3(a, t[u].c.y, t[u].c.z, t[u].c.x);
+                R.n2[i] = sel3(a, t[u].c.z, t[u].c.x, t[u].c.y);
+                R.vl[i] = (unsigned char)vl;
+                atomicAdd(&s_cnt[vl], 1);
+                double rv[7];
+#ifdef FA_EXP_NOVALUES
+                for (int j2 = 0; j2 < 7; ++j2) rv[j2] = 1.0 + j2;
+#else
+                record_values<KIND>(A, t[u], a, s_oq[vl], s_ow[vl], rv);
+#endif
+#pragma unroll
+                for (int j2 = 0; j2 < RVALS; ++j2) R.vals[j2 * CAPB + i] = rv[j2];
+            }
+        }
+    }
     __syncthreads();
+    // ---- b) counting sort by vertex ---------------------------------------------------------
     {
         const int c = tid < BV ? s_cnt[tid] : 0;
         const int64_t ex = block_exclusive_scan<NT>(int64_t(c), s_warp, &s_total);
         if (tid < BV) s_start[tid] = int(ex);
     }
     __syncthreads();
-    if (!overflow) {
-        for (int64_t i = tid; i < n; i += NT) {
-            const int vl = brec[i].w >> 2;
-            s_idx[s_start[vl] + atomicAdd(&s_fill[vl], 1)] = (unsigned short)i;
-        }
+    for (int i = tid; i < n; i += NT) {
+        const int vl = R.vl[i];
+        R.list[s_start[vl] + atomicAdd(&s_fill[vl], 1)] = (unsigned short)i;
     }
     __syncthreads();
 
     const int vloc = tid / RPV, s = tid % RPV;
-    const int64_t v = A.v0 + b * BV + vloc;
+    const int64_t v = vbase + vloc;
     const bool active = v < A.v1;
     const int64_t r = (b * BV + vloc) * RPV + s;  // local matrix row
     const int deg = active ? s_cnt[vloc] : 0;
     const int start = active ? s_start[vloc] : 0;
     const bool slow = active && (deg > MAXD || overflow);
-    OwnVertex own;
-    own.v = v;
-    own.p = make_double2(0.0, 0.0);
-    own.w = 0.0;
-    if (active) {
-        if (TR::NEED_Q || A.areas == nullptr) own.p = A.q[v];
-        if (TR::NEED_W) own.w = A.w[v];
-    }
-    BucketView B{brec, n, s_idx, overflow};
-    int64_t count = 0, drops = 0;
     const bool any_slow = __syncthreads_or(slow);
 
-    // ---- general path, counting phase ----------------------------------------------------
-    if (any_slow && slow) count = general_row<KIND>(A, B, start, deg, vloc, own, s, 0, false, &drops);
-
-    // ---- fast path: <= MAXD incidences in registers --------------------------------------
-    bool spilled = false;
-    if (active && !slow) {
-        uint4 rr[MAXD];
+    // ---- c) fast rows: records into registers ----------------------------------------------
+    int nb[NC];
+    double ov[NC][NV];
+    double dsum[NV];
 #pragma unroll
-        for (int i = 0; i < MAXD; ++i)
-            rr[i] = i < deg ? brec[s_idx[start + i]] : make_uint4(0xffffffffu, 0xffffffffu, 0xffffffffu, 0);
-        sort8(rr);
-        int nb[NC];
-        double ov[NC][NV];
-        double dsum[NV];
+    for (int t = 0; t < NV; ++t) dsum[t] = 0.0;
+    const bool fast = active && !slow;
+    if (fast) {
+        uint64_t sk[MAXD];
 #pragma unroll
-        for (int t = 0; t < NV; ++t) dsum[t] = 0.0;
+        for (int i = 0; i < MAXD; ++i) {
+            if (i < deg) {
+                const int ridx = R.list[start + i];
+                sk[i] = (uint64_t(R.key[ridx]) << 16) | uint64_t(ridx);
+            } else {
+                sk[i] = ~uint64_t(0);
+            }
+        }
+        sort8(sk);
 #pragma unroll
         for (int i = 0; i < MAXD; ++i) {
             double d[2], o1[2], o2[2];
             if (i < deg) {
-                row_values<KIND>(A, own, rr[i], s, d, o1, o2);
-                nb[2 * i] = int(rr[i].y);
-                nb[2 * i + 1] = int(rr[i].z);
+                const int ridx = int(sk[i] & 0xffff);
+                const int a = int((sk[i] >> 16) & 3);
+                double rv[7];
+#pragma unroll
+                for (int j = 0; j < RVALS; ++j) rv[j] = R.vals[j * CAPB + ridx];
+                record_row<KIND>(A, rv, a, s, d, o1, o2);
+                nb[2 * i] = R.n1[ridx];
+                nb[2 * i + 1] = R.n2[ridx];
             } else {
                 nb[2 * i] = INT_MAX;
                 nb[2 * i + 1] = INT_MAX;
@@ -452,9 +594,25 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, 1) k_rows(RowsArgs 
                 ov[2 * i + 1][t] = o2[t];
             }
         }
-        // merge: vertex columns in ascending order (the row's own vertex included)
-        const int vv = int(v);
+    } else {
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+            nb[j] = INT_MAX;
+#pragma unroll
+            for (int t = 0; t < NV; ++t) ov[j][t] = 0.0;
+        }
+    }
+    int64_t count = 0, drops = 0;
+    if (slow) count = general_row<KIND>(A, R, overflow, start, deg, v, s, 0, false, &drops);
+    // staging is only used when no row of the bucket needs the records afterwards
+    const bool stage = !any_slow;
+    __syncthreads();  // every row holds its data: the records area becomes the staging area
+
+    // merge: vertex columns in ascending order (the row's own vertex included)
+    const int vv = int(v);
+    auto merge = [&](bool to_global, int64_t out_pos) -> int64_t {
         int last = -1;
+        int64_t cnt = 0;
         double* my_val = s_val + tid * STRIDE;
         int32_t* my_col = s_col + tid * STRIDE;
         while (true) {
@@ -478,27 +636,45 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, 1) k_rows(RowsArgs 
 #pragma unroll
             for (int t = 0; t < NV; ++t) {
                 if (sum[t] != 0.0) {
-                    if (count < CAPR) {
-                        my_col[count] = NV == 1 ? c : 2 * c + t;
-                        my_val[count] = sum[t];
+                    const int cc = NV == 1 ? c : 2 * c + t;
+                    if (to_global) {
+                        if (out_pos + cnt < A.capacity) {
+                            A.col[out_pos + cnt] = cc;
+                            A.val[out_pos + cnt] = sum[t];
+                        }
+                    } else if (stage && cnt < CAPR) {
+                        my_col[cnt] = cc;
+                        my_val[cnt] = sum[t];
                     }
-                    ++count;
-                } else {
+                    ++cnt;
+                } else if (!to_global) {
                     ++drops;
                 }
             }
             last = c;
         }
-        spilled = count > CAPR;
-    }
-    s_slow[tid] = (slow || spilled) ? 1 : 0;
-    const bool any_spilled = __syncthreads_or(spilled);
+        return cnt;
+    };
+#ifdef FA_EXP_NOMERGE
+    if (fast) count = deg;
+#else
+    if (fast) count = merge(false, 0);  // writes staging only when `stage` (see below)
+#endif
+    const bool spilled = fast && count > CAPR;
+    const bool direct = __syncthreads_or(spilled) || !stage;
 
-    // ---- block scan + look-back: global offset of this bucket's first row ----------------
+    // ---- d) block scan + look-back: global offset of this bucket's first row -------------
     const int64_t excl = block_exclusive_scan<NT>(count, s_warp, &s_total);
     s_off[tid] = excl;
     if (tid == NT - 1) s_off[NT] = excl + count;
+    if (!direct)
+        for (int64_t j = 0; j < count; ++j) s_owner[excl + j] = (unsigned short)tid;  // staged entries' row
+#ifdef FA_EXP_NOLOOKBACK
+    __syncthreads();
+    const uint64_t base = uint64_t(b) * CAPB;
+#else
     const uint64_t base = lookback_prefix(A.status, b, uint64_t(s_total), &s_prefix);
+#endif
     const int64_t total = s_total;
 
     if (active) A.rowptr[r] = int64_t(base) + excl;
@@ -509,37 +685,34 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, 1) k_rows(RowsArgs 
     if (drops) atomicAdd(reinterpret_cast<unsigned long long*>(&A.res->dropped), (unsigned long long)drops);
     if (slow) atomicAdd(reinterpret_cast<unsigned long long*>(&A.res->heavy_rows), 1ull);
 
-    // ---- coalesced copy-out of the staged segment ----------------------------------------
-    const bool check_slow = any_slow || any_spilled;
-    for (int64_t e = tid; e < total; e += NT) {
-        int lt = 0, ht = NT;  // largest t with s_off[t] <= e
-        while (ht - lt > 1) {
-            const int mid = (lt + ht) >> 1;
-            if (s_off[mid] <= e) lt = mid; else ht = mid;
+    if (!direct) {
+        // coalesced copy-out of the staged segment (owner of each entry from s_owner)
+        for (int64_t e = tid; e < total; e += NT) {
+            const int lt = s_owner[e];
+            const int j = int(e - s_off[lt]);
+            const int64_t g = int64_t(base) + e;
+            if (g < A.capacity) {
+                A.col[g] = s_col[lt * STRIDE + j];
+                A.val[g] = s_val[lt * STRIDE + j];
+            }
         }
-        if (check_slow && s_slow[lt]) continue;
-        const int j = int(e - s_off[lt]);
-        const int64_t g = int64_t(base) + e;
-        if (g < A.capacity) {
-            A.col[g] = s_col[lt * STRIDE + j];
-            A.val[g] = s_val[lt * STRIDE + j];
-        }
+    } else {
+        if (fast) merge(true, int64_t(base) + excl);
+        if (slow) general_row<KIND>(A, R, overflow, start, deg, v, s, int64_t(base) + excl, true, nullptr);
     }
-    // ---- rows that did not fit the staging area or need the general path ---------------
-    if (spilled || slow) general_row<KIND>(A, B, start, deg, vloc, own, s, int64_t(base) + excl, true, nullptr);
 }
 
-template <int KIND>
-constexpr size_t rows_smem_bytes() {
-    return size_t(KindTraits<KIND>::THREADS) * KindTraits<KIND>::STRIDE * (sizeof(double) + sizeof(int32_t));
-}
+// Optional CUDA events recorded around the row kernel (bench.py's per-kernel roofline).
+static thread_local cudaEvent_t g_timer_begin = nullptr, g_timer_end = nullptr;
 
 template <int KIND>
 static int launch_rows(const RowsArgs& A, int64_t nbuckets, cudaStream_t st) {
-    const size_t smem = rows_smem_bytes<KIND>();
+    const size_t smem = RowsSmem<KIND>::bytes;
     FA_CUDA(cudaFuncSetAttribute(k_rows<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    if (g_timer_begin) FA_CUDA(cudaEventRecord(g_timer_begin, st));
     k_rows<KIND><<<dim3(unsigned(nbuckets)), KindTraits<KIND>::THREADS, smem, st>>>(A);
     FA_LAUNCH_CHECK("k_rows");
+    if (g_timer_end) FA_CUDA(cudaEventRecord(g_timer_end, st));
     return FA_OK;
 }
 
@@ -552,13 +725,11 @@ struct fa_plan {
     int device;
     int64_t nme, nq, v0, v1, nb, chunk;
     const int32_t* me;
-    int* bcount;              // nb + 1
-    int64_t* bptr;            // nb + 1
-    unsigned* bcursor;        // nb
-    uint4* rec;               // up to 3*nme incidence records
-    uint64_t* status;         // look-back tile status
+    unsigned* bfill;          // nb
+    unsigned* keys;           // nb * CAPB
+    fa::TriRec* T;            // per-triangle records (allocated on first assembly)
+    uint64_t* status;         // look-back tile status (nb)
     unsigned long long* ticket;
-    int64_t status_len;
     int64_t ninc;             // -1 until read back
     bool built;
 };
@@ -566,8 +737,7 @@ struct fa_plan {
 using namespace fa;
 
 static void plan_free(fa_plan* p) {
-    cudaFree(p->bcount); cudaFree(p->bptr); cudaFree(p->bcursor); cudaFree(p->rec);
-    cudaFree(p->status); cudaFree(p->ticket);
+    cudaFree(p->bfill); cudaFree(p->keys); cudaFree(p->T); cudaFree(p->status); cudaFree(p->ticket);
 }
 
 extern "C" int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t row_begin, int64_t row_end) {
@@ -588,19 +758,17 @@ extern "C" int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t ro
     p->nme = nme; p->nq = nq; p->v0 = row_begin; p->v1 = row_end;
     const int64_t nv = row_end - row_begin;
     p->nb = (nv + BV - 1) / BV;
-    // enough triangles per block that each bucket sees a few records per block
-    int64_t chunk = 4096;
-    while (chunk * 3 < 4 * p->nb && chunk < (int64_t(1) << 20)) chunk *= 2;
+    // triangles per scatter block: enough that each bucket sees several keys per block,
+    // at most 16384 (u16 shared counters), at least a few blocks per SM
+    int64_t chunk = 2048;
+    while (chunk < 16384 && chunk * 3 < 6 * p->nb && (nme + 2 * chunk - 1) / (2 * chunk) >= 2 * NUM_SMS_B200) chunk *= 2;
     p->chunk = chunk;
-    const int64_t scan_tiles = (p->nb + SCAN_BLOCK * SCAN_ITEMS - 1) / (SCAN_BLOCK * SCAN_ITEMS) + 1;
-    p->status_len = (scan_tiles > p->nb ? scan_tiles : p->nb) + 1;
     p->ninc = -1;
     cudaError_t e = cudaSuccess;
-    if (e == cudaSuccess) e = cudaMalloc(&p->bcount, sizeof(int) * (p->nb + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&p->bptr, sizeof(int64_t) * (p->nb + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&p->bcursor, sizeof(unsigned) * (p->nb + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&p->rec, sizeof(uint4) * 3 * nme);
-    if (e == cudaSuccess) e = cudaMalloc(&p->status, sizeof(uint64_t) * p->status_len);
+    const int64_t nbk = p->nb > 0 ? p->nb : 1;
+    if (e == cudaSuccess) e = cudaMalloc(&p->bfill, sizeof(unsigned) * nbk);
+    if (e == cudaSuccess) e = cudaMalloc(&p->keys, sizeof(unsigned) * size_t(nbk) * CAPB);
+    if (e == cudaSuccess) e = cudaMalloc(&p->status, sizeof(uint64_t) * nbk);
     if (e == cudaSuccess) e = cudaMalloc(&p->ticket, sizeof(unsigned long long));
     if (e != cudaSuccess) {
         plan_free(p);
@@ -625,32 +793,26 @@ extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, 
     p->ninc = -1;
     p->built = true;
     k_reset_result<<<1, 32, 0, st>>>(d_res);
-    FA_CUDA(cudaMemsetAsync(p->bcount, 0, sizeof(int) * (p->nb + 1), st));
-    FA_CUDA(cudaMemsetAsync(p->bcursor, 0, sizeof(unsigned) * (p->nb + 1), st));
-    PlanArgs P{d_me, p->nme, p->nq, p->v0, p->v1, p->nb, p->chunk, p->bcount, p->bptr, p->bcursor, p->rec, d_res};
+    if (p->nb == 0) return FA_OK;
+    FA_CUDA(cudaMemsetAsync(p->bfill, 0, sizeof(unsigned) * p->nb, st));
+    PlanArgs P{d_me, p->nme, p->nq, p->v0, p->v1, p->nb, p->chunk, p->bfill, p->keys, d_res};
     const unsigned blocks = unsigned((p->nme + p->chunk - 1) / p->chunk);
-    const bool smem = p->nb <= SMEM_NB;
-    const size_t hist_bytes = smem ? sizeof(int) * size_t(p->nb) : 0;
-    if (smem) {
-        FA_CUDA(cudaFuncSetAttribute(k_bucket_count<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_bytes)));
-        FA_CUDA(cudaFuncSetAttribute(k_bucket_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_bytes)));
-        k_bucket_count<true><<<blocks, PLAN_BLOCK, hist_bytes, st>>>(P);
+    if (p->nb <= SMEM_NB) {
+        const size_t hist_bytes = sizeof(unsigned) * size_t((p->nb + 1) / 2);
+        FA_CUDA(cudaFuncSetAttribute(k_plan_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_bytes)));
+        k_plan_scatter<true><<<blocks, PLAN_BLOCK, hist_bytes, st>>>(P);
     } else {
-        k_bucket_count<false><<<blocks, PLAN_BLOCK, 0, st>>>(P);
+        k_validate_ids<<<grid_for(3 * p->nme, 256), 256, 0, st>>>(d_me, 3 * p->nme, p->nq, d_res);
+        FA_LAUNCH_CHECK("k_validate_ids");
+        k_plan_scatter<false><<<blocks, PLAN_BLOCK, 0, st>>>(P);
     }
-    FA_LAUNCH_CHECK("k_bucket_count");
-    if (p->nb == 0) {
-        FA_CUDA(cudaMemsetAsync(p->bptr, 0, sizeof(int64_t), st));
-        return FA_OK;
-    }
-    const int64_t tiles = (p->nb + SCAN_BLOCK * SCAN_ITEMS - 1) / (SCAN_BLOCK * SCAN_ITEMS);
-    FA_CUDA(cudaMemsetAsync(p->status, 0, sizeof(uint64_t) * (tiles + 1), st));
-    FA_CUDA(cudaMemsetAsync(p->ticket, 0, sizeof(unsigned long long), st));
-    k_scan_i32_to_i64<<<dim3(unsigned(tiles)), SCAN_BLOCK, 0, st>>>(p->bcount, p->nb, p->bptr, p->status, p->ticket);
-    FA_LAUNCH_CHECK("k_scan_i32_to_i64");
-    if (smem) k_bucket_scatter<true><<<blocks, PLAN_BLOCK, hist_bytes, st>>>(P);
-    else k_bucket_scatter<false><<<blocks, PLAN_BLOCK, 0, st>>>(P);
-    FA_LAUNCH_CHECK("k_bucket_scatter");
+    FA_LAUNCH_CHECK("k_plan_scatter");
+    return FA_OK;
+}
+
+extern "C" int fa_set_kernel_timer(void* ev_begin, void* ev_end) {
+    g_timer_begin = reinterpret_cast<cudaEvent_t>(ev_begin);
+    g_timer_end = reinterpret_cast<cudaEvent_t>(ev_end);
     return FA_OK;
 }
 
@@ -667,7 +829,15 @@ extern "C" int fa_plan_capacity(fa_plan* p, int kind, int64_t* capacity) {
         if (p->v0 == 0 && p->v1 == p->nq) {
             p->ninc = 3 * p->nme;  // every corner is owned
         } else {
-            FA_CUDA(cudaMemcpy(&p->ninc, p->bptr + p->nb, sizeof(int64_t), cudaMemcpyDeviceToHost));
+            // keys written to the row block's buckets (bfill may exceed CAPB: still exact counts)
+            unsigned* h = static_cast<unsigned*>(malloc(sizeof(unsigned) * size_t(p->nb > 0 ? p->nb : 1)));
+            if (!h) { set_error("out of host memory"); return FA_ERR_ARGUMENT; }
+            cudaError_t e = cudaMemcpy(h, p->bfill, sizeof(unsigned) * p->nb, cudaMemcpyDeviceToHost);
+            if (e != cudaSuccess) { free(h); return cuda_status(e, "fa_plan_capacity"); }
+            int64_t s = 0;
+            for (int64_t i = 0; i < p->nb; ++i) s += h[i];
+            free(h);
+            p->ninc = s;
         }
     }
     // per vertex: at most 2*deg neighbours + itself; ELASTIC: 2 rows x 2 columns per vertex
@@ -686,6 +856,7 @@ extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double
         set_error("fa_assemble: vertex coordinates required"); return FA_ERR_ARGUMENT;
     }
     if (kind == FA_KIND_MASSW && !d_w) { set_error("WEIGHTED_MASS requires a WeightField"); return FA_ERR_ARGUMENT; }
+    if (kind == FA_KIND_MASSW && !d_areas) { set_error("WEIGHTED_MASS requires areas"); return FA_ERR_ARGUMENT; }
     cudaStream_t st = as_stream(stream);
     const int64_t nrows = fa_plan_rows(p, kind);
     k_reset_result<<<1, 32, 0, st>>>(d_res);
@@ -693,11 +864,23 @@ extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double
         FA_CUDA(cudaMemsetAsync(d_rowptr, 0, sizeof(int64_t), st));
         return FA_OK;
     }
+    if (!p->T) FA_CUDA(cudaMalloc(&p->T, sizeof(TriRec) * p->nme));
+    {
+        const int gb = grid_for(p->nme, 256);
+        const double2* q2 = reinterpret_cast<const double2*>(d_q);
+        switch (kind) {
+            case FA_KIND_MASS: k_tri_records<FA_KIND_MASS><<<gb, 256, 0, st>>>(p->me, p->nme, q2, d_areas, p->T, d_res); break;
+            case FA_KIND_MASSW: k_tri_records<FA_KIND_MASSW><<<gb, 256, 0, st>>>(p->me, p->nme, q2, d_areas, p->T, d_res); break;
+            case FA_KIND_STIFF: k_tri_records<FA_KIND_STIFF><<<gb, 256, 0, st>>>(p->me, p->nme, q2, d_areas, p->T, d_res); break;
+            default: k_tri_records<FA_KIND_ELASTIC><<<gb, 256, 0, st>>>(p->me, p->nme, q2, d_areas, p->T, d_res); break;
+        }
+        FA_LAUNCH_CHECK("k_tri_records");
+    }
     FA_CUDA(cudaMemsetAsync(p->status, 0, sizeof(uint64_t) * p->nb, st));
     FA_CUDA(cudaMemsetAsync(p->ticket, 0, sizeof(unsigned long long), st));
     RowsArgs A;
-    A.bptr = p->bptr; A.rec = p->rec;
-    A.q = reinterpret_cast<const double2*>(d_q); A.areas = d_areas; A.w = d_w;
+    A.keys = p->keys; A.bfill = p->bfill; A.me = p->me; A.nme = p->nme;
+    A.q = reinterpret_cast<const double2*>(d_q); A.areas = d_areas; A.w = d_w; A.T = p->T;
     A.lam = lam; A.mu = mu;
     A.v0 = p->v0; A.v1 = p->v1; A.nrows = nrows;
     A.rowptr = d_rowptr; A.col = d_col; A.val = d_val; A.capacity = capacity;
