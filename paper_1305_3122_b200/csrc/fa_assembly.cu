@@ -181,10 +181,11 @@ struct alignas(32) TriRec {
 template <int KIND>
 __global__ void k_tri_records(const int32_t* __restrict__ me, int64_t nme, const double2* __restrict__ q,
                               const double* __restrict__ areas, TriRec* __restrict__ T, fa_result* res) {
+    const uint64_t pol = l2_evict_first_policy();
     for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nme; k += int64_t(gridDim.x) * blockDim.x) {
-        int c0, c1, c2;
-        load_tri_ids(me, k, c0, c1, c2);
-        const double area = areas ? areas[k] : tri_area(q[c0], q[c1], q[c2]);
+        const int c0 = ld_stream_i32(me + 3 * k, pol), c1 = ld_stream_i32(me + 3 * k + 1, pol),
+                  c2 = ld_stream_i32(me + 3 * k + 2, pol);
+        const double area = areas ? ld_stream_f64(areas + k, pol) : tri_area(q[c0], q[c1], q[c2]);
         if (KIND != FA_KIND_MASSW && area <= AREA_EPS) atomic_min_i64(&res->degenerate_index, k);
         TriRec t;
         t.c = make_int4(c0, c1, c2, 0);
@@ -451,6 +452,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, 1) k_rows(RowsArgs 
     __shared__ unsigned short s_owner[NT * CAPR];
 
     const int tid = threadIdx.x;
+    const uint64_t pol_first = l2_evict_first_policy();
     const int64_t b = next_tile(A.ticket, &s_tile);  // bucket, in launch order
     const unsigned filled = A.bfill[b];
     const bool overflow = filled > unsigned(CAPB);
@@ -472,7 +474,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, 1) k_rows(RowsArgs 
     //         cooperatively and swaps halves), neighbour data, its row values -> shared memory.
     //         AU rounds are issued together so each warp keeps several loads in flight.
     {
-        constexpr int AU = 3;
+        constexpr int AU = 6;
         const int lane = tid & 31, warp = tid >> 5, half = lane & 1, pair = lane >> 1;
         const uint4* T4 = reinterpret_cast<const uint4*>(A.T);
         for (int base0 = warp * 32; base0 < n; base0 += NT * AU) {
@@ -485,7 +487,8 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, 1) k_rows(RowsArgs 
                 const int base = base0 + u * NT;
                 const int iA = base + pair, iB = base + 16 + pair;
                 const bool okA = iA < n, okB = iB < n;
-                const unsigned keyA = okA ? bkeys[iA] : 0u, keyB = okB ? bkeys[iB] : 0u;
+                const unsigned keyA = okA ? ld_stream_u32(bkeys + iA, pol_first) : 0u;
+                const unsigned keyB = okB ? ld_stream_u32(bkeys + iB, pol_first) : 0u;
                 la[u] = okA ? T4[2 * int64_t(keyA >> 2) + half] : make_uint4(0u, 0u, 0u, 0u);
                 lb[u] = okB ? T4[2 * int64_t(keyB >> 2) + half] : make_uint4(0u, 0u, 0u, 0u);
                 key[u] = half ? keyB : keyA;  // even lane keeps record A, odd lane record B
@@ -528,6 +531,10 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, 1) k_rows(RowsArgs 
         }
     }
     __syncthreads();
+#ifdef FA_EXP_STOP_A
+    if (tid == 0 && n == 12345) A.res->reserved[0] = R.key[0];
+    return;
+#endif
     // ---- b) counting sort by vertex ---------------------------------------------------------
     {
         const int c = tid < BV ? s_cnt[tid] : 0;
@@ -541,6 +548,10 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, 1) k_rows(RowsArgs 
     }
     __syncthreads();
 
+#ifdef FA_EXP_STOP_B
+    if (tid == 0 && n == 12345) A.res->reserved[0] = R.list[0];
+    return;
+#endif
     const int vloc = tid / RPV, s = tid % RPV;
     const int64_t v = vbase + vloc;
     const bool active = v < A.v1;
@@ -660,6 +671,10 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, 1) k_rows(RowsArgs 
 #else
     if (fast) count = merge(false, 0);  // writes staging only when `stage` (see below)
 #endif
+#ifdef FA_EXP_STOP_C
+    if (count == 12345) A.res->reserved[0] = count;
+    return;
+#endif
     const bool spilled = fast && count > CAPR;
     const bool direct = __syncthreads_or(spilled) || !stage;
 
@@ -677,7 +692,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, 1) k_rows(RowsArgs 
 #endif
     const int64_t total = s_total;
 
-    if (active) A.rowptr[r] = int64_t(base) + excl;
+    if (active) st_stream_i64(A.rowptr + r, int64_t(base) + excl, pol_first);
     if (active && r == A.nrows - 1) {
         A.rowptr[A.nrows] = int64_t(base) + excl + count;
         A.res->nnz = int64_t(base) + excl + count;
@@ -692,8 +707,8 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, 1) k_rows(RowsArgs 
             const int j = int(e - s_off[lt]);
             const int64_t g = int64_t(base) + e;
             if (g < A.capacity) {
-                A.col[g] = s_col[lt * STRIDE + j];
-                A.val[g] = s_val[lt * STRIDE + j];
+                st_stream_i32(A.col + g, s_col[lt * STRIDE + j], pol_first);
+                st_stream_f64(A.val + g, s_val[lt * STRIDE + j], pol_first);
             }
         }
     } else {

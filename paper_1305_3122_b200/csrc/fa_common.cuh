@@ -52,11 +52,36 @@ __device__ __forceinline__ void st_volatile_u64(uint64_t* p, uint64_t v) {
     asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
 
-// Streaming (read-once) loads: keep them from evicting the gathered working set in L2.
-__device__ __forceinline__ uint32_t ld_stream_u32(const uint32_t* p) {
-    uint32_t v;
-    asm volatile("ld.global.L1::no_allocate.L2::evict_first.u32 %0, [%1];" : "=r"(v) : "l"(p));
+// Streaming accesses (read or written once) carry an L2 evict-first policy so they do not
+// displace the randomly gathered working set (triangle records, q, w) from L2.
+__device__ __forceinline__ uint64_t l2_evict_first_policy() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ unsigned ld_stream_u32(const unsigned* p, uint64_t pol) {
+    unsigned v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
     return v;
+}
+__device__ __forceinline__ int ld_stream_i32(const int* p, uint64_t pol) {
+    int v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ld_stream_f64(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ void st_stream_i32(int* p, int v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.s32 [%0], %1, %2;" ::"l"(p), "r"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_stream_i64(int64_t* p, int64_t v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.s64 [%0], %1, %2;" ::"l"(p), "l"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void st_stream_f64(double* p, double v, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
 
 template <typename T>

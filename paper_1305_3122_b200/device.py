@@ -50,6 +50,8 @@ def to_device(arr: np.ndarray, dtype=None):
     """Upload a numpy array (contiguous) to the current CUDA device."""
     torch = require_cuda()
     a = np.ascontiguousarray(arr if dtype is None else arr.astype(dtype, copy=False))
+    if not a.flags.writeable:  # frozen Mesh arrays: torch.from_numpy needs a writable buffer
+        a = a.copy()
     return torch.from_numpy(a).to(device(), non_blocking=False)
 
 

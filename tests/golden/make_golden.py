@@ -117,7 +117,11 @@ def digests(names):
     path = HERE / "reference_digests.json"
     data = json.loads(path.read_text()) if path.exists() else {}
     for spec in names:
-        # spec: C1 | C1:s1 | EL64 (elastic lam=2 mu=0.7 N=64 seed 0)
+        # spec: C1 | C1:s1 | EL64 (elastic lam=2 mu=0.7 N=64 seed 0) | C5B:G:b (row block b of G)
+        if spec.startswith("C5B"):
+            _, g, blk = spec.split(":")
+            row_block_digest(data, path, "C5", int(g), int(blk), seed=0)
+            continue
         if spec.startswith("EL64"):
             kind, n, lam, mu, seeds = "elastic", 64, 2.0, 0.7, [0]
             cfg = "EL64"
@@ -147,6 +151,35 @@ def digests(names):
             print(key, data[key]["nnz"], f"{t1 - t0:.1f}s", flush=True)
             path.write_text(json.dumps(data, indent=1, sort_keys=True))
             del mesh, m, sm
+
+
+def row_block_digest(data, path, cfg, G, blk, seed=0):
+    """Reference output restricted to vertex rows [v0, v1) of block blk of G, obtained with
+    the row-block subset: the triangles touching the block, in their
+    original order, assembled by femasm; the block's CSC columns equal the full assembly's."""
+    kind, n, lam, mu = BASELINE_CONFIGS[cfg]
+    t0 = time.perf_counter()
+    sm = seeded_square_mesh(n, seed)
+    nq = sm.nq
+    v0, v1 = (nq * blk) // G, (nq * (blk + 1)) // G
+    C = sm.connectivity
+    touch = ((C >= v0) & (C < v1)).any(axis=1)
+    sub = femasm.Mesh(sm.vertices, C[touch])
+    m = femasm.assemble(sub, KIND[kind], femasm.Strategy.OPTV2)
+    lo, hi = int(m.col_ptr[v0]), int(m.col_ptr[v1])
+    ptr = m.col_ptr[v0:v1 + 1] - lo
+    key = f"{cfg}B/s{seed}/G{G}/b{blk}"
+    data[key] = {
+        "kind": kind, "N": n, "seed": seed, "G": G, "block": blk, "v0": int(v0), "v1": int(v1),
+        "nq": int(nq), "nme": int(sm.nme), "touched": int(touch.sum()), "nnz": int(hi - lo),
+        "mesh_sha256": mesh_digest(sm),
+        "col_ptr_sha256": digest(ptr.astype("<i8")),
+        "row_idx_sha256": digest(m.row_idx[lo:hi].astype("<i8")),
+        "values_sha256": digest(m.values[lo:hi].astype("<f8")),
+        "reference_seconds": round(time.perf_counter() - t0, 2),
+    }
+    print(key, data[key]["nnz"], data[key]["reference_seconds"], flush=True)
+    path.write_text(json.dumps(data, indent=1, sort_keys=True))
 
 
 if __name__ == "__main__":

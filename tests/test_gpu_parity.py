@@ -74,9 +74,26 @@ def test_reference_digests(digests, key):
 
 
 @pytest.mark.slow
-@pytest.mark.parametrize("key", ["C3/s0", "C4/s0", "C3/s1", "C4/s1"])
+@pytest.mark.parametrize("key", ["C3/s0", "C3/s1", "C3/s2", "C4/s0", "C4/s1", "C4/s2"])
 def test_reference_digests_large(digests, key):
+    """Full BASELINE sizes (8.4M triangles) against the reference's own output digests;
+    C4 seeds differ in how many elasticity positions cancel to exactly 0.0."""
     test_reference_digests(digests, key)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("key", ["C5B/s0/G16/b0", "C5B/s0/G8/b7"])
+def test_c5_row_block_digest(digests, key):
+    """N=8192 (134M triangles): one GPU assembles the vertex-row block of a G-way
+    decomposition; the reference digest is the row-block subset assembled by femasm."""
+    if key not in digests:
+        pytest.skip("digest not generated")
+    d = digests[key]
+    sm = seeded_square_mesh(d["N"], d["seed"])
+    areas = c_oracle.areas(sm.vertices, sm.connectivity)
+    got, r = plan_assemble(d["kind"], sm.vertices, sm.connectivity, areas, sm.weights, 1.0, 0.5, d["v0"], d["v1"])
+    assert r.nnz == d["nnz"]
+    assert csc_digests(*got) == (d["col_ptr_sha256"], d["row_idx_sha256"], d["values_sha256"])
 
 
 @pytest.mark.parametrize("kind", KINDS)
