@@ -1,35 +1,39 @@
-// OptV2 assembly on B200: fixed-capacity vertex-bucket plan + fused row kernel (element
-// values, Matlab sparse() summation, zero drop, row offsets, CSR write) for one block of
-// vertex rows.
+// OptV2 assembly on B200: vertex-sorted incidence plan + fused row kernel (element values,
+// Matlab sparse() summation, zero drop, row offsets, CSR write) for one block of vertex rows.
 //
 // Reference path replaced (pkg/src/femasm): assemble(..., OPTV2) assembly.py:419-452 ->
 // _assemble_batched :400-416 -> build_ig_jg_p1[_vector] :162-192 + batch_kg_* :214-307 ->
 // TripletBatch.to_csc sparse.py:318-329 -> csc_from_triplets :140-189.
 //
-// Design:
-//   plan    K1 scatter   vertices are grouped in buckets of BV consecutive ids, each with room
-//                        for CAPB incidence keys (8 per vertex).  One pass over the
-//                        connectivity writes key = (k << 2) | a for every (triangle k, corner
-//                        a) into its vertex's bucket; slots come from shared-memory histograms
-//                        plus one global atomic per (block, bucket).  The key array (32 B per
-//                        vertex) is small enough to stay in L2 while it is scattered.
-//   numeric K2 records   one 32-byte record per triangle {c0, c1, c2, area or (area/6,
-//                        area/12)}, coalesced, so an incidence costs one L1 line below.
-//           K3 rows      one block per bucket:
-//                        a) every key of the bucket (balanced over threads): gather the
-//                           triangle record (lane pairs, one L1 line per record) and the
-//                           neighbours' q or w, compute that row of its element matrix
-//                           bit-exactly (values, or the gradients for elasticity) into
-//                           shared memory;
-//                        b) counting sort of the records by vertex in shared memory;
-//                        c) one thread per matrix row: its <= MAXD records sorted by k in
-//                           registers, columns merged in ascending order with each position
-//                           summed sequentially in ascending k (== stable argsort + bincount of
-//                           the reference), exact-zero sums dropped;
-//                        d) block scan + decoupled look-back for the global row offset, the
-//                           bucket's CSR segment staged in shared memory and written coalesced.
-// Rows with more than MAXD incidences, and buckets that overflowed CAPB, take a general
-// O(d^2) path (the latter scanning the connectivity) and write directly to global memory.
+// Design.  Vertex and triangle numbering are arbitrary (the benchmark meshes are
+// randomly permuted), so every access keyed by the "other" index is a random gather.  The plan
+// turns the connectivity into per-vertex incidence lists that carry everything the numeric
+// pass needs except floating-point data, so the numeric pass gathers only from the small,
+// L2-resident arrays (areas 8 B/triangle, q 16 B/vertex, w 8 B/vertex):
+//   plan (symbolic, reads `me` only)
+//     K1 part_hist   owned incidences per part (PV consecutive vertices) - shared-memory
+//                    histogram, one global atomic per (block, part)
+//     K2 part_scan   part offsets
+//     K3 part_place  per round of triangles: incidence records {k, vertex-in-part<<2|a, n1, n2}
+//                    ranked by part in shared memory, one range reserved per (round, part),
+//                    written as coalesced runs
+//     K4 part_sort   per part: counting sort by vertex in shared memory, each vertex's list
+//                    sorted by k; written as SoA (k<<2|a, n1, n2) + per-vertex offsets ivptr
+//   numeric
+//     K5 rows        one block per bucket of BV vertices:
+//                    a) per incidence (balanced over threads): plan entry (coalesced), the
+//                       triangle area and neighbour q / w (gathers from L2-resident arrays),
+//                       the row of the element matrix computed bit-exactly into shared memory
+//                       (gradients + area for elasticity);
+//                    c) one thread per matrix row: its <= MAXD incidences are contiguous and in
+//                       ascending k; the 2*deg neighbour columns are sorted with a 16-key
+//                       odd-even merge network; a linear pass sums every position sequentially
+//                       in ascending k (== stable argsort + bincount of the reference) and
+//                       drops exact-zero sums;
+//                    d) block scan + decoupled look-back for the global row offset; the
+//                       bucket's CSR segment is staged in shared memory and written coalesced.
+// Rows of degree > MAXD (and every row of a bucket whose incidences exceed CAPB) use an
+// O(d^2) general path with the same summation order.
 #include <climits>
 #include <cstdlib>
 #include <new>
@@ -37,14 +41,21 @@
 #include "fa_common.cuh"
 #include "fa_element.cuh"
 
+#ifndef FA_ROWS_MINB
+#define FA_ROWS_MINB 4  // scalar kinds: <= 128 registers, no local memory
+#endif
+
 namespace fa {
 
-constexpr int BV = 128;          // vertices per bucket
-constexpr int CAPB = 8 * BV;     // key slots per bucket
-constexpr int MAXD = 8;          // incidences per row on the register fast path
-constexpr int SMEM_NB = 32768;   // buckets counted with (u16-packed) shared-memory histograms
-constexpr int PLAN_BLOCK = 1024;
-constexpr int PLAN_UNROLL = 4;
+constexpr int BV = 128;            // vertices per row bucket
+constexpr int CAPB = 8 * BV;       // incidences per bucket held in shared memory
+constexpr int MAXD = 8;            // incidences per row on the register fast path
+constexpr int PLOG0 = 10;          // log2 of the minimum part size (vertices)
+constexpr int MAX_PARTS = 8192;
+constexpr int PLAN_THREADS = 1024;
+constexpr int SORT_THREADS = 512;   // k_part_sort (2 blocks / SM, 64 registers)
+constexpr int PLACE_TRI = 2048;    // triangles per placement round
+constexpr int SORT_CAP = 7680;     // part incidences sorted in shared memory (2 blocks / SM)
 
 __global__ void k_reset_result(fa_result* r) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
@@ -59,161 +70,317 @@ __global__ void k_reset_result(fa_result* r) {
     }
 }
 
-// ------------------------------------------------------------------------------------------
-// plan: one scatter pass
-// ------------------------------------------------------------------------------------------
-struct PlanArgs {
-    const int32_t* me;
-    int64_t nme, nq, v0, v1;
-    int64_t nb;          // buckets
-    int64_t chunk;       // triangles per block
-    unsigned* bfill;     // nb: keys written (may exceed CAPB: overflow)
-    unsigned* keys;      // nb * CAPB
-    fa_result* res;
-};
-
 __device__ __forceinline__ void load_tri_ids(const int32_t* me, int64_t k, int& c0, int& c1, int& c2) {
     c0 = me[3 * k];
     c1 = me[3 * k + 1];
     c2 = me[3 * k + 2];
 }
 
-template <bool SMEM>
-__global__ void __launch_bounds__(PLAN_BLOCK) k_plan_scatter(PlanArgs P) {
-    extern __shared__ unsigned s_cnt[];  // u16 pairs: count, then running slot
-    const int64_t k0 = blockIdx.x * P.chunk;
-    const int64_t k1 = min(P.nme, k0 + P.chunk);
-    constexpr int STEP = PLAN_BLOCK * PLAN_UNROLL;
-    if (SMEM) {
-        for (int64_t w = threadIdx.x; w < (P.nb + 1) / 2; w += PLAN_BLOCK) s_cnt[w] = 0;
-        __syncthreads();
-        for (int64_t kb = k0 + threadIdx.x; kb < k1; kb += STEP) {
-            int c[PLAN_UNROLL][3];
-#pragma unroll
-            for (int u = 0; u < PLAN_UNROLL; ++u) {
-                const int64_t k = kb + int64_t(u) * PLAN_BLOCK;
-                if (k < k1) load_tri_ids(P.me, k, c[u][0], c[u][1], c[u][2]);
-                else c[u][0] = c[u][1] = c[u][2] = -1;
-            }
-#pragma unroll
-            for (int u = 0; u < PLAN_UNROLL; ++u)
-#pragma unroll
-                for (int a = 0; a < 3; ++a) {
-                    const int64_t v = c[u][a];
-                    const int64_t k = kb + int64_t(u) * PLAN_BLOCK;
-                    if (k >= k1) continue;
-                    if (v < 0 || v >= P.nq) {
-                        atomic_min_i64(&P.res->index_error_pos, 3 * k + a);
-                        continue;
-                    }
-                    if (v < P.v0 || v >= P.v1) continue;
-                    const int64_t b = (v - P.v0) / BV;
-                    atomicAdd(&s_cnt[b >> 1], 1u << ((b & 1) * 16));
-                }
-        }
-        __syncthreads();
-        // reserve slots: one global atomic per (block, bucket); keep the base (<= CAPB) in place
-        for (int64_t w = threadIdx.x; w < (P.nb + 1) / 2; w += PLAN_BLOCK) {
-            const unsigned pair = s_cnt[w];
-            unsigned out = 0;
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                const unsigned c = (pair >> (16 * h)) & 0xffffu;
-                const int64_t b = 2 * w + h;
-                if (c && b < P.nb) {
-                    const unsigned base = atomicAdd(&P.bfill[b], c);
-                    out |= min(base, unsigned(CAPB)) << (16 * h);
-                }
-            }
-            s_cnt[w] = out;
-        }
-        __syncthreads();
-    }
-    for (int64_t kb = k0 + threadIdx.x; kb < k1; kb += STEP) {
-        int c[PLAN_UNROLL][3];
-#pragma unroll
-        for (int u = 0; u < PLAN_UNROLL; ++u) {
-            const int64_t k = kb + int64_t(u) * PLAN_BLOCK;
-            if (k < k1) load_tri_ids(P.me, k, c[u][0], c[u][1], c[u][2]);
-            else c[u][0] = c[u][1] = c[u][2] = -1;
-        }
-#pragma unroll
-        for (int u = 0; u < PLAN_UNROLL; ++u)
-#pragma unroll
-            for (int a = 0; a < 3; ++a) {
-                const int64_t v = c[u][a];
-                const int64_t k = kb + int64_t(u) * PLAN_BLOCK;
-                if (k >= k1 || v < P.v0 || v >= P.v1 || v >= P.nq) continue;
-                const int64_t b = (v - P.v0) / BV;
-                unsigned pos;
-                if (SMEM) {
-                    const int sh = int(b & 1) * 16;
-                    pos = (atomicAdd(&s_cnt[b >> 1], 1u << sh) >> sh) & 0xffffu;
-                } else {
-                    if (!SMEM && v < 0) continue;
-                    pos = atomicAdd(&P.bfill[b], 1u);
-                }
-                if (pos < CAPB) P.keys[b * CAPB + pos] = (unsigned(k) << 2) | unsigned(a);
-            }
-    }
-}
-
-// index validation for the global-atomic path is done here (k_plan_scatter<false> only
-// stores in-range keys and cannot report without a second branch in the hot loop)
-__global__ void k_validate_ids(const int32_t* __restrict__ me, int64_t n3, int64_t nq, fa_result* res) {
-    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n3; i += int64_t(gridDim.x) * blockDim.x) {
-        const int v = me[i];
-        if (v < 0 || v >= nq) atomic_min_i64(&res->index_error_pos, i);
-    }
-}
-
 // ------------------------------------------------------------------------------------------
-// numeric K2: one 32-byte record per triangle {c0, c1, c2, -, x, y} so that a row kernel
-// incidence costs a single L1 line: x, y = area/6, area/12 (mass, assembly.py:219-220) or
-// x = area (other kinds; recomputed from q with compute_areas' formula when areas is NULL).
-// The degeneracy check of assembly.py:152-155 runs here once per triangle.
+// plan
 // ------------------------------------------------------------------------------------------
-struct alignas(32) TriRec {
-    int4 c;      // c0, c1, c2, unused
-    double2 v;   // kind-specific values
+struct PlanArgs {
+    const int32_t* me;
+    int64_t nme, nq, v0, v1;
+    int plog;               // part = (v - v0) >> plog
+    int nparts;
+    int64_t chunk;          // triangles per block of K1 / K3
+    unsigned* part_off;     // nparts + 1: counts (K1), exclusive offsets (K2)
+    unsigned* part_fill;    // nparts: placement cursors
+    unsigned* M;            // [blocks][nparts]: owned incidences of each K1/K3 block per part
+    uint4* rec;             // owned incidences grouped by part {k, vp << 2 | a, n1, n2}
+    unsigned* skey;         // sorted by (vertex, k): k << 2 | a
+    unsigned* sn1;          // neighbour at corner a+1
+    unsigned* sn2;          // neighbour at corner a+2
+    unsigned* ivptr;        // nv + 1: first incidence of every owned vertex
+    fa_result* res;
 };
 
-template <int KIND>
-__global__ void k_tri_records(const int32_t* __restrict__ me, int64_t nme, const double2* __restrict__ q,
-                              const double* __restrict__ areas, TriRec* __restrict__ T, fa_result* res) {
-    const uint64_t pol = l2_evict_first_policy();
-    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nme; k += int64_t(gridDim.x) * blockDim.x) {
-        const int c0 = ld_stream_i32(me + 3 * k, pol), c1 = ld_stream_i32(me + 3 * k + 1, pol),
-                  c2 = ld_stream_i32(me + 3 * k + 2, pol);
-        const double area = areas ? ld_stream_f64(areas + k, pol) : tri_area(q[c0], q[c1], q[c2]);
-        if (KIND != FA_KIND_MASSW && area <= AREA_EPS) atomic_min_i64(&res->degenerate_index, k);
-        TriRec t;
-        t.c = make_int4(c0, c1, c2, 0);
-        if (KIND == FA_KIND_MASS) {
-            const MassTri m = mass_prepare(area);
-            t.v = make_double2(m.d, m.o);
-        } else {
-            t.v = make_double2(area, 0.0);
+// K1: owned incidences per (block, part) and per part; index validation (sparse.py:131-137 semantics: first bad
+// position in the flattened connectivity).
+__global__ void __launch_bounds__(PLAN_THREADS) k_part_hist(const __grid_constant__ PlanArgs P) {
+    extern __shared__ unsigned s_cnt[];
+    for (int i = threadIdx.x; i < P.nparts; i += PLAN_THREADS) s_cnt[i] = 0;
+    __syncthreads();
+    const int64_t k0 = int64_t(blockIdx.x) * P.chunk, k1 = min(P.nme, k0 + P.chunk);
+    for (int64_t k = k0 + threadIdx.x; k < k1; k += PLAN_THREADS) {
+        int c[3];
+        load_tri_ids(P.me, k, c[0], c[1], c[2]);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+            const int64_t v = c[a];
+            if (v < 0 || v >= P.nq) {
+                atomic_min_i64(&P.res->index_error_pos, 3 * k + a);
+                continue;
+            }
+            if (v >= P.v0 && v < P.v1) atomicAdd(&s_cnt[(v - P.v0) >> P.plog], 1u);
         }
-        T[k] = t;
+    }
+    __syncthreads();
+    unsigned* row = P.M + int64_t(blockIdx.x) * P.nparts;
+    for (int i = threadIdx.x; i < P.nparts; i += PLAN_THREADS) {
+        row[i] = s_cnt[i];
+        if (s_cnt[i]) atomicAdd(&P.part_off[i], s_cnt[i]);
+    }
+}
+
+// K2: exclusive scan of the part counts (one block; nparts <= MAX_PARTS = 8 per thread).
+__global__ void __launch_bounds__(PLAN_THREADS) k_part_scan(const __grid_constant__ PlanArgs P) {
+    __shared__ unsigned s_warp[PLAN_THREADS / 32];
+    __shared__ unsigned s_total;
+    constexpr int PER = MAX_PARTS / PLAN_THREADS;
+    unsigned c[PER], run = 0;
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int i = threadIdx.x * PER + j;
+        c[j] = i < P.nparts ? P.part_off[i] : 0u;
+        run += c[j];
+    }
+    unsigned ex = block_exclusive_scan<PLAN_THREADS>(run, s_warp, &s_total);
+#pragma unroll
+    for (int j = 0; j < PER; ++j) {
+        const int i = threadIdx.x * PER + j;
+        if (i < P.nparts) {
+            P.part_off[i] = ex;
+            P.part_fill[i] = ex;
+        }
+        ex += c[j];
+    }
+    if (threadIdx.x == 0) P.part_off[P.nparts] = s_total;
+}
+
+// K3: incidence records grouped by part.  Each block reserves its range in every part once
+// (count matrix row of K1, one atomic per part); per round of PLACE_TRI triangles the records
+// are ranked by part in shared memory, staged in part order and written as coalesced runs.
+// Order inside a part is arbitrary (K4 sorts).
+__global__ void __launch_bounds__(PLAN_THREADS, 1) k_part_place(const __grid_constant__ PlanArgs P) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int RI = 3 * PLACE_TRI;                  // incidences per round
+    constexpr int TPT = PLACE_TRI / PLAN_THREADS;      // triangles per thread per round
+    uint4* s_stage = reinterpret_cast<uint4*>(smem_raw);                    // [RI]
+    unsigned* s_cnt = reinterpret_cast<unsigned*>(s_stage + RI);            // [nparts] round counts
+    unsigned* s_lst = s_cnt + P.nparts;                                     // [nparts] round local starts
+    unsigned* s_gb = s_lst + P.nparts;                                      // [nparts] global cursor
+    unsigned short* s_part = reinterpret_cast<unsigned short*>(s_gb + P.nparts);  // [RI]
+    __shared__ unsigned s_warp[PLAN_THREADS / 32];
+    __shared__ unsigned s_total;
+    const int tid = threadIdx.x;
+    const int64_t kb0 = int64_t(blockIdx.x) * P.chunk, kb1 = min(P.nme, kb0 + P.chunk);
+    const int pmask = (1 << P.plog) - 1;
+    {
+        const unsigned* row = P.M + int64_t(blockIdx.x) * P.nparts;
+        for (int i = tid; i < P.nparts; i += PLAN_THREADS) {
+            const unsigned c = row[i];
+            s_gb[i] = c ? atomicAdd(&P.part_fill[i], c) : 0u;
+        }
+    }
+    for (int64_t r0 = kb0; r0 < kb1; r0 += PLACE_TRI) {
+        for (int i = tid; i < P.nparts; i += PLAN_THREADS) s_cnt[i] = 0;
+        __syncthreads();
+        uint4 rec[3 * TPT];
+        unsigned part[3 * TPT], rank[3 * TPT];
+#pragma unroll
+        for (int t = 0; t < TPT; ++t) {
+            const int64_t k = r0 + t * PLAN_THREADS + tid;
+            int c[3] = {-1, -1, -1};
+            if (k < kb1) load_tri_ids(P.me, k, c[0], c[1], c[2]);
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const int64_t v = c[a];
+                const int j = 3 * t + a;
+                part[j] = 0xffffffffu;
+                if (v >= P.v0 && v < P.v1 && v < P.nq) {
+                    const unsigned vl = unsigned(v - P.v0);
+                    part[j] = vl >> P.plog;
+                    rank[j] = atomicAdd(&s_cnt[part[j]], 1u);
+                    rec[j] = make_uint4(unsigned(k), ((vl & unsigned(pmask)) << 2) | unsigned(a),
+                                        unsigned(sel3(a, c[1], c[2], c[0])), unsigned(sel3(a, c[2], c[0], c[1])));
+                }
+            }
+        }
+        __syncthreads();
+        // local starts: exclusive scan of the round counts over parts
+        constexpr int PER = MAX_PARTS / PLAN_THREADS;
+        unsigned cl[PER], run = 0;
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = tid * PER + j;
+            cl[j] = i < P.nparts ? s_cnt[i] : 0u;
+            run += cl[j];
+        }
+        unsigned ex = block_exclusive_scan<PLAN_THREADS>(run, s_warp, &s_total);
+#pragma unroll
+        for (int j = 0; j < PER; ++j) {
+            const int i = tid * PER + j;
+            if (i < P.nparts) s_lst[i] = ex;
+            ex += cl[j];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < 3 * TPT; ++j) {
+            if (part[j] != 0xffffffffu) {
+                const unsigned pos = s_lst[part[j]] + rank[j];
+                s_stage[pos] = rec[j];
+                s_part[pos] = (unsigned short)part[j];
+            }
+        }
+        __syncthreads();
+        const int total = int(s_total);
+        for (int i = tid; i < total; i += PLAN_THREADS) {
+            const unsigned p = s_part[i];
+            const unsigned g = s_gb[p] + (unsigned(i) - s_lst[p]);
+            const uint4 r = s_stage[i];
+            asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(P.rec + g), "r"(r.x),
+                         "r"(r.y), "r"(r.z), "r"(r.w)
+                         : "memory");
+        }
+        __syncthreads();
+        for (int i = tid; i < P.nparts; i += PLAN_THREADS) s_gb[i] += s_cnt[i];
+    }
+}
+
+// Sort one vertex's incidences by key (k << 2 | a, unique) with their neighbours: insertion
+// sort for short lists, heapsort beyond (O(d log d), in place).
+__device__ void sort_incidences(unsigned* key, unsigned* n1, unsigned* n2, int d) {
+    if (d <= 32) {
+        for (int i = 1; i < d; ++i) {
+            const unsigned x = key[i], y1 = n1[i], y2 = n2[i];
+            int j = i - 1;
+            while (j >= 0 && key[j] > x) {
+                key[j + 1] = key[j];
+                n1[j + 1] = n1[j];
+                n2[j + 1] = n2[j];
+                --j;
+            }
+            key[j + 1] = x;
+            n1[j + 1] = y1;
+            n2[j + 1] = y2;
+        }
+        return;
+    }
+    auto sift = [&](int root, int end) {
+        while (true) {
+            int child = 2 * root + 1;
+            if (child >= end) break;
+            if (child + 1 < end && key[child + 1] > key[child]) ++child;
+            if (key[root] >= key[child]) break;
+            unsigned t = key[root]; key[root] = key[child]; key[child] = t;
+            t = n1[root]; n1[root] = n1[child]; n1[child] = t;
+            t = n2[root]; n2[root] = n2[child]; n2[child] = t;
+            root = child;
+        }
+    };
+    for (int i = d / 2 - 1; i >= 0; --i) sift(i, d);
+    for (int end = d - 1; end > 0; --end) {
+        unsigned t = key[0]; key[0] = key[end]; key[end] = t;
+        t = n1[0]; n1[0] = n1[end]; n1[end] = t;
+        t = n2[0]; n2[0] = n2[end]; n2[end] = t;
+        sift(0, end);
+    }
+}
+
+// K4: one block per part.  Counting sort by vertex, every vertex's list by k; SoA output and
+// per-vertex offsets.  Parts of PV == 1024 vertices and up to SORT_CAP incidences are sorted
+// in shared memory, others in place in global memory.  s_cur[v]: count, then start, then
+// (after placement) end of vertex v.
+__global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_constant__ PlanArgs P) {
+    extern __shared__ __align__(16) unsigned s_dyn[];
+    __shared__ unsigned s_warp[SORT_THREADS / 32];
+    __shared__ unsigned s_total;
+    const int p = blockIdx.x, tid = threadIdx.x;
+    const int PV = 1 << P.plog;
+    const int64_t nv = P.v1 - P.v0;
+    const int64_t vfirst = int64_t(p) << P.plog;
+    const int nvp = int(min(int64_t(PV), nv - vfirst));
+    const unsigned off = P.part_off[p], n = P.part_off[p + 1] - off;
+    const bool fast = PV == (1 << PLOG0) && n <= unsigned(SORT_CAP);
+    unsigned* s_cur = s_dyn;  // [PV]
+    const uint64_t pol = l2_evict_first_policy();
+    for (int i = tid; i < PV; i += SORT_THREADS) s_cur[i] = 0;
+    __syncthreads();
+    for (unsigned i = tid; i < n; i += SORT_THREADS) atomicAdd(&s_cur[P.rec[off + i].y >> 2], 1u);
+    __syncthreads();
+    // vertex starts: thread t scans PV / 1024 consecutive vertices
+    const int per = PV / SORT_THREADS;
+    unsigned run = 0;
+    for (int j = 0; j < per; ++j) run += s_cur[tid * per + j];
+    unsigned ex = block_exclusive_scan<SORT_THREADS>(run, s_warp, &s_total);
+    for (int j = 0; j < per; ++j) {
+        const int v = tid * per + j;
+        const unsigned c = s_cur[v];
+        s_cur[v] = ex;
+        if (v < nvp) P.ivptr[vfirst + v] = off + ex;
+        ex += c;
+    }
+    if (p == P.nparts - 1 && tid == 0) P.ivptr[nv] = off + n;
+    __syncthreads();
+    unsigned* key = fast ? s_dyn + PV : P.skey + off;
+    unsigned* n1 = fast ? s_dyn + PV + SORT_CAP : P.sn1 + off;
+    unsigned* n2 = fast ? s_dyn + PV + 2 * SORT_CAP : P.sn2 + off;
+    unsigned short* s_src = reinterpret_cast<unsigned short*>(s_dyn + PV + 3 * SORT_CAP);  // fast: [SORT_CAP]
+    for (unsigned i = tid; i < n; i += SORT_THREADS) {
+        uint4 r;
+        asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
+                     : "l"(P.rec + off + i), "l"(pol));
+        const unsigned pos = atomicAdd(&s_cur[r.y >> 2], 1u);
+        key[pos] = (r.x << 2) | (r.y & 3u);
+        n1[pos] = r.z;
+        n2[pos] = r.w;
+    }
+    __syncthreads();
+    if (fast) {
+        // per vertex: rank of every incidence among the vertex's keys (unique) -> source slot
+        // of every sorted position; then one coalesced permuting copy
+        for (int v = tid; v < PV; v += SORT_THREADS) {
+        const unsigned st = v ? s_cur[v - 1] : 0u, d = s_cur[v] - st;
+        if (d <= 8) {
+            unsigned kk[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) kk[j] = j < int(d) ? key[st + j] : 0xffffffffu;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+                if (i < int(d)) {
+                    unsigned r = 0;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) r += kk[j] < kk[i] ? 1u : 0u;
+                    s_src[st + r] = (unsigned short)(st + i);
+                }
+            }
+        } else {
+            sort_incidences(key + st, n1 + st, n2 + st, int(d));
+            for (unsigned i = 0; i < d; ++i) s_src[st + i] = (unsigned short)(st + i);
+        }
+        }
+        __syncthreads();
+        for (unsigned i = tid; i < n; i += SORT_THREADS) {
+            const unsigned j = s_src[i];
+            P.skey[off + i] = key[j];
+            P.sn1[off + i] = n1[j];
+            P.sn2[off + i] = n2[j];
+        }
+    } else {
+        for (int v = tid; v < PV; v += SORT_THREADS) {
+            const unsigned st = v ? s_cur[v - 1] : 0u, d = s_cur[v] - st;
+            if (d > 1) sort_incidences(key + st, n1 + st, n2 + st, int(d));
+        }
     }
 }
 
 // ------------------------------------------------------------------------------------------
-// row kernel
+// numeric: rows
 // ------------------------------------------------------------------------------------------
 struct RowsArgs {
-    const unsigned* keys;
-    const unsigned* bfill;
-    const int32_t* me;
-    int64_t nme;
+    const unsigned* skey;   // sorted (vertex, k): k << 2 | a
+    const unsigned* sn1;
+    const unsigned* sn2;
+    const unsigned* ivptr;  // nv + 1
     const double2* q;
-    const double* areas;  // nullable: recompute from q (bitwise compute_areas)
     const double* w;
-    const TriRec* T;      // per-triangle records (k_tri_records)
+    const double* areas;    // nullable: recompute from q (bitwise compute_areas)
     double lam, mu;
-    int64_t v0, v1;       // owned vertices
-    int64_t nrows;        // matrix rows produced (owned vertices * rows per vertex)
+    int64_t v0, v1;         // owned vertices
+    int64_t nrows;          // matrix rows produced (owned vertices * rows per vertex)
     int64_t* rowptr;
     int32_t* col;
     double* val;
@@ -227,185 +394,190 @@ template <int KIND>
 struct KindTraits {
     static constexpr int RPV = KIND == FA_KIND_ELASTIC ? 2 : 1;  // rows per vertex
     static constexpr int NV = KIND == FA_KIND_ELASTIC ? 2 : 1;   // values per (row, vertex column)
-    static constexpr bool CHECK_AREA = KIND != FA_KIND_MASSW;   // massw never checks (assembly.py:227-243)
     static constexpr int THREADS = BV * RPV;
-    static constexpr int CAPR = KIND == FA_KIND_ELASTIC ? 16 : 2 * MAXD + 1;  // staged entries per row
-    static constexpr int STRIDE = CAPR | 1;                                   // odd: conflict-free
     // per-record shared data: scalar kinds store the row's three values, elasticity the
-    // triangle's gradients + area (entries are formed per dof row in the merge phase)
+    // triangle's gradients + area (entries are formed per dof row in the merge)
     static constexpr int RVALS = KIND == FA_KIND_ELASTIC ? 7 : 3;
+    static constexpr int MIN_BLOCKS = KIND == FA_KIND_ELASTIC ? 2 : FA_ROWS_MINB;
+    static constexpr size_t REC_BYTES = size_t(CAPB) * (RVALS * 8 + 8);
+    static constexpr int STAGE = int(REC_BYTES / 12);  // staged entries fitting the records area
 };
 
-// Shared-memory layout of the row kernel (records area and staging area are unioned).
 template <int KIND>
-struct RowsSmem {
-    using TR = KindTraits<KIND>;
-    static constexpr size_t rec_bytes = size_t(CAPB) * (TR::RVALS * 8 + 4 + 4 + 4 + 2 + 1);
-    static constexpr size_t stage_bytes = size_t(TR::THREADS) * TR::STRIDE * 12;
-    static constexpr size_t bytes = (rec_bytes > stage_bytes ? rec_bytes : stage_bytes) + 64;
+constexpr size_t rows_smem_bytes() {
+    return KindTraits<KIND>::REC_BYTES;
+}
+
+// Gathered data of one incidence: neighbour coordinates / weights and the triangle area.
+struct Gathered {
+    double2 p1, p2;
+    double w1, w2, ar;
 };
 
-// Values of one record: the element-matrix row of corner a against the triangle's vertices
-// in local order (own, n1, n2).  Elasticity: gradients + area instead.  `own_p` / `own_w`
-// are the own vertex's coordinates / weight (from shared memory), n1 / n2 data is gathered.
 template <int KIND>
-__device__ __forceinline__ void record_values(const RowsArgs& A, const TriRec& t, int a, double2 own_p, double own_w,
-                                              double* out) {
-    const int b1 = a == 2 ? 0 : a + 1, b2 = a == 0 ? 2 : a - 1;
-    const int n1 = sel3(a, t.c.y, t.c.z, t.c.x), n2 = sel3(a, t.c.z, t.c.x, t.c.y);
+__device__ __forceinline__ Gathered gather_incidence(const RowsArgs& A, unsigned k, unsigned n1, unsigned n2) {
+    Gathered g;
+    g.p1 = g.p2 = make_double2(0.0, 0.0);
+    g.w1 = g.w2 = 0.0;
+    g.ar = A.areas ? A.areas[k] : 0.0;
+    if (KIND == FA_KIND_STIFF || KIND == FA_KIND_ELASTIC || !A.areas) {
+        g.p1 = A.q[n1];
+        g.p2 = A.q[n2];
+    }
+    if (KIND == FA_KIND_MASSW) {
+        g.w1 = A.w[n1];
+        g.w2 = A.w[n2];
+    }
+    return g;
+}
+
+// Values of one incidence: row a of the element matrix against the triangle's vertices in
+// local order (own, n1, n2); elasticity: gradients + area instead.  Degenerate triangles are
+// reported (assembly.py:152-155) for every kind that divides by the area.
+template <int KIND>
+__device__ __forceinline__ void incidence_values(const RowsArgs& A, unsigned k, int a, const Gathered& g,
+                                                 double2 own_p, double own_w, double* out) {
+    const double2 c0 = sel3(a, own_p, g.p2, g.p1), c1 = sel3(a, g.p1, own_p, g.p2), c2 = sel3(a, g.p2, g.p1, own_p);
+    const double ar = A.areas ? g.ar : tri_area(c0, c1, c2);
+    if (KIND != FA_KIND_MASSW && ar <= AREA_EPS) atomic_min_i64(&A.res->degenerate_index, int64_t(k));
     if constexpr (KIND == FA_KIND_MASS) {
-        out[0] = t.v.x;
-        out[1] = t.v.y;
-        out[2] = t.v.y;
+        const MassTri m = mass_prepare(ar);
+        out[0] = m.d;
+        out[1] = m.o;
+        out[2] = m.o;
     } else if constexpr (KIND == FA_KIND_MASSW) {
-        const double w1 = A.w[n1], w2 = A.w[n2];
-        const MasswTri m = massw_prepare(t.v.x, sel3(a, own_w, w2, w1), sel3(a, w1, own_w, w2), sel3(a, w2, w1, own_w));
+        const MasswTri m = massw_prepare(ar, sel3(a, own_w, g.w2, g.w1), sel3(a, g.w1, own_w, g.w2), sel3(a, g.w2, g.w1, own_w));
         // row a against (a, a+1, a+2): a=0 -> (e00, e10, e20), a=1 -> (e11, e21, e10), a=2 -> (e22, e20, e21)
         out[0] = sel3(a, m.e00, m.e11, m.e22);
         out[1] = sel3(a, m.e10, m.e21, m.e20);
         out[2] = sel3(a, m.e20, m.e10, m.e21);
-    } else {
-        const double2 p1 = A.q[n1], p2 = A.q[n2];
-        const double2 c0 = sel3(a, own_p, p2, p1), c1 = sel3(a, p1, own_p, p2), c2 = sel3(a, p2, p1, own_p);
-        if constexpr (KIND == FA_KIND_STIFF) {
-            const StiffTri m = stiff_prepare(c0, c1, c2, t.v.x);
-            out[0] = stiff_entry(m, a, a);
-            out[1] = stiff_entry(m, a, b1);
-            out[2] = stiff_entry(m, a, b2);
-        } else {
-            const ElasticTri m = elastic_prepare(c0, c1, c2, t.v.x);
-            out[0] = m.g0.x; out[1] = m.g0.y;
-            out[2] = m.g1.x; out[3] = m.g1.y;
-            out[4] = m.g2.x; out[5] = m.g2.y;
-            out[6] = m.area;
-        }
-    }
-}
-
-// The three (x NV) values of dof row s of a record: at the own vertex, n1, n2.
-template <int KIND>
-__device__ __forceinline__ void record_row(const RowsArgs& A, const double* rv, int a, int s, double (&d)[2],
-                                           double (&o1)[2], double (&o2)[2]) {
-    if constexpr (KIND == FA_KIND_ELASTIC) {
-        ElasticTri t;
-        t.g0 = make_double2(rv[0], rv[1]);
-        t.g1 = make_double2(rv[2], rv[3]);
-        t.g2 = make_double2(rv[4], rv[5]);
-        t.area = rv[6];
-        const double P = FADD(A.lam, FMUL(2.0, A.mu));
+    } else if constexpr (KIND == FA_KIND_STIFF) {
         const int b1 = a == 2 ? 0 : a + 1, b2 = a == 0 ? 2 : a - 1;
-        const int i = 2 * a + s;
-#pragma unroll
-        for (int tt = 0; tt < 2; ++tt) {
-            d[tt] = elastic_entry(t, i, 2 * a + tt, A.lam, A.mu, P);
-            o1[tt] = elastic_entry(t, i, 2 * b1 + tt, A.lam, A.mu, P);
-            o2[tt] = elastic_entry(t, i, 2 * b2 + tt, A.lam, A.mu, P);
-        }
+        const StiffTri m = stiff_prepare(c0, c1, c2, ar);
+        out[0] = stiff_entry(m, a, a);
+        out[1] = stiff_entry(m, a, b1);
+        out[2] = stiff_entry(m, a, b2);
     } else {
-        d[0] = rv[0];
-        o1[0] = rv[1];
-        o2[0] = rv[2];
-        d[1] = o1[1] = o2[1] = 0.0;
+        const ElasticTri m = elastic_prepare(c0, c1, c2, ar);
+        out[0] = m.g0.x; out[1] = m.g0.y;
+        out[2] = m.g1.x; out[3] = m.g1.y;
+        out[4] = m.g2.x; out[5] = m.g2.y;
+        out[6] = m.area;
     }
 }
 
-__device__ __forceinline__ void cswap64(uint64_t& x, uint64_t& y) {
-    const uint64_t lo = x < y ? x : y, hi = x < y ? y : x;
+// Entry of an incidence from its values: dof row s (x/y of the own vertex for elasticity),
+// column vertex rel (0 = own, 1 = n1, 2 = n2), column component t.
+template <int KIND>
+__device__ __forceinline__ double entry_from(const RowsArgs& A, const double* rv, int a, int s, int rel, int t) {
+    if constexpr (KIND == FA_KIND_ELASTIC) {
+        ElasticTri m;
+        m.g0 = make_double2(rv[0], rv[1]);
+        m.g1 = make_double2(rv[2], rv[3]);
+        m.g2 = make_double2(rv[4], rv[5]);
+        m.area = rv[6];
+        const double P = FADD(A.lam, FMUL(2.0, A.mu));
+        const int bl = rel == 0 ? a : (rel == 1 ? (a == 2 ? 0 : a + 1) : (a == 0 ? 2 : a - 1));
+        return elastic_entry(m, 2 * a + s, 2 * bl + t, A.lam, A.mu, P);
+    } else {
+        return rel == 0 ? rv[0] : (rel == 1 ? rv[1] : rv[2]);
+    }
+}
+
+// Same from the shared record of slot `slot`.
+template <int KIND>
+__device__ __forceinline__ double record_entry(const RowsArgs& A, const double* vals, int slot, int a, int s,
+                                               int rel, int t) {
+    if constexpr (KIND == FA_KIND_ELASTIC) {
+        double rv[7];
+#pragma unroll
+        for (int j = 0; j < 7; ++j) rv[j] = vals[j * CAPB + slot];
+        return entry_from<KIND>(A, rv, a, s, rel, t);
+    } else {
+        return vals[rel * CAPB + slot];
+    }
+}
+
+__device__ __forceinline__ void cs(unsigned& x, unsigned& y) {
+    const unsigned lo = min(x, y), hi = max(x, y);
     x = lo;
     y = hi;
 }
-// optimal 19-comparator network for 8 keys (verified by the 0-1 principle)
-__device__ __forceinline__ void sort8(uint64_t (&k)[8]) {
-    cswap64(k[0], k[2]); cswap64(k[1], k[3]); cswap64(k[4], k[6]); cswap64(k[5], k[7]);
-    cswap64(k[0], k[4]); cswap64(k[1], k[5]); cswap64(k[2], k[6]); cswap64(k[3], k[7]);
-    cswap64(k[0], k[1]); cswap64(k[2], k[3]); cswap64(k[4], k[5]); cswap64(k[6], k[7]);
-    cswap64(k[2], k[4]); cswap64(k[3], k[5]);
-    cswap64(k[1], k[4]); cswap64(k[3], k[6]);
-    cswap64(k[1], k[2]); cswap64(k[3], k[4]); cswap64(k[5], k[6]);
+// Batcher odd-even merge sort, 16 keys, 63 comparators (verified by the 0-1 principle)
+__device__ __forceinline__ void sort16(unsigned (&k)[16]) {
+    cs(k[0], k[1]); cs(k[2], k[3]); cs(k[0], k[2]); cs(k[1], k[3]); cs(k[1], k[2]); cs(k[4], k[5]); cs(k[6], k[7]); cs(k[4], k[6]);
+    cs(k[5], k[7]); cs(k[5], k[6]); cs(k[0], k[4]); cs(k[2], k[6]); cs(k[2], k[4]); cs(k[1], k[5]); cs(k[3], k[7]); cs(k[3], k[5]);
+    cs(k[1], k[2]); cs(k[3], k[4]); cs(k[5], k[6]); cs(k[8], k[9]); cs(k[10], k[11]); cs(k[8], k[10]); cs(k[9], k[11]); cs(k[9], k[10]);
+    cs(k[12], k[13]); cs(k[14], k[15]); cs(k[12], k[14]); cs(k[13], k[15]); cs(k[13], k[14]); cs(k[8], k[12]); cs(k[10], k[14]); cs(k[10], k[12]);
+    cs(k[9], k[13]); cs(k[11], k[15]); cs(k[11], k[13]); cs(k[9], k[10]); cs(k[11], k[12]); cs(k[13], k[14]); cs(k[0], k[8]); cs(k[4], k[12]);
+    cs(k[4], k[8]); cs(k[2], k[10]); cs(k[6], k[14]); cs(k[6], k[10]); cs(k[2], k[4]); cs(k[6], k[8]); cs(k[10], k[12]); cs(k[1], k[9]);
+    cs(k[5], k[13]); cs(k[5], k[9]); cs(k[3], k[11]); cs(k[7], k[15]); cs(k[7], k[11]); cs(k[3], k[5]); cs(k[7], k[9]); cs(k[11], k[13]);
+    cs(k[1], k[2]); cs(k[3], k[4]); cs(k[5], k[6]); cs(k[7], k[8]); cs(k[9], k[10]); cs(k[11], k[12]); cs(k[13], k[14]);
 }
 
-// Records of one bucket in shared memory.
+// Shared records of one bucket.
 struct BucketRecs {
-    unsigned* key;            // (k << 2) | a
-    int* n1;
-    int* n2;
-    double* vals;             // [RVALS][CAPB]
-    unsigned short* list;     // record indices grouped by vertex
-    unsigned char* vl;        // vertex (local) of each record
+    double* vals;          // [RVALS][CAPB]
+    int* n1;               // [CAPB]
+    int* n2;               // [CAPB]
+    unsigned char* a;      // [CAPB] local corner of the row's vertex
 };
 
-// General path for one row: O(d^2) selection with the same summation order (ascending k
-// per position).  In-smem records (`overflow` false) or, for an overflowed bucket, a scan of
-// the whole connectivity.  Writes only when `write`.
+struct RowCount {
+    int64_t count, drops;
+};
+
+// General path for one row: O(d^2) selection with the same summation order (ascending k per
+// position).  Incidences from shared memory (slots start..start+deg, ascending k) or, when the
+// bucket did not fit (overflow), from the plan in global memory (positions gfirst.., same
+// order) with the values recomputed.  Writes when `write`.
 template <int KIND>
-__device__ int64_t general_row(const RowsArgs& A, const BucketRecs& R, bool overflow, int start, int deg,
-                               int64_t v, int s, int64_t out_pos, bool write, int64_t* drops) {
+__device__ __noinline__ RowCount general_row(const RowsArgs& A, BucketRecs R, bool overflow, int64_t gfirst, int start,
+                                             int deg, int64_t v, double2 own_p, double own_w, int s, int64_t out_pos,
+                                             bool write) {
     constexpr int NV = KindTraits<KIND>::NV;
     constexpr int RVALS = KindTraits<KIND>::RVALS;
-    const int64_t m = overflow ? A.nme : deg;
-    // incidence i of the row: triangle k, local corner a, other corners n1, n2
-    auto get = [&](int64_t i, int64_t& k, int& a, int& n1, int& n2, int& ridx) -> bool {
+    auto get = [&](int i, int& a, int& n1, int& n2, double* rv, bool need_vals) {
         if (!overflow) {
-            ridx = R.list[start + i];
-            const unsigned key = R.key[ridx];
-            k = key >> 2;
-            a = key & 3;
-            n1 = R.n1[ridx];
-            n2 = R.n2[ridx];
-            return true;
+            const int slot = start + i;
+            a = R.a[slot];
+            n1 = R.n1[slot];
+            n2 = R.n2[slot];
+            if (need_vals)
+                for (int j = 0; j < RVALS; ++j) rv[j] = R.vals[j * CAPB + slot];
+            return;
         }
-        int c0, c1, c2;
-        load_tri_ids(A.me, i, c0, c1, c2);
-        if (c0 == v) a = 0; else if (c1 == v) a = 1; else if (c2 == v) a = 2; else return false;
-        k = i;
-        n1 = sel3(a, c1, c2, c0);
-        n2 = sel3(a, c2, c0, c1);
-        ridx = -1;
-        return true;
+        const unsigned ka = A.skey[gfirst + i];
+        a = int(ka & 3u);
+        n1 = int(A.sn1[gfirst + i]);
+        n2 = int(A.sn2[gfirst + i]);
+        if (need_vals) {
+            const Gathered g = gather_incidence<KIND>(A, ka >> 2, unsigned(n1), unsigned(n2));
+            incidence_values<KIND>(A, ka >> 2, a, g, own_p, own_w, rv);
+        }
     };
-    int64_t last = -1, count = 0;
+    int64_t last = -1, count = 0, drops = 0;
     while (true) {
         int64_t c = INT64_MAX;  // next vertex column
         if (v > last) c = v;
-        for (int64_t i = 0; i < m; ++i) {
-            int64_t k; int a, n1, n2, ridx;
-            if (!get(i, k, a, n1, n2, ridx)) continue;
+        for (int i = 0; i < deg; ++i) {
+            int a, n1, n2;
+            get(i, a, n1, n2, nullptr, false);
             if (n1 > last && n1 < c) c = n1;
             if (n2 > last && n2 < c) c = n2;
         }
         if (c == INT64_MAX) break;
         double sum[NV];
-#pragma unroll
         for (int t = 0; t < NV; ++t) sum[t] = 0.0;
-        int64_t prevk = -1;
-        while (true) {  // contributions to column c in ascending k
-            int64_t bestk = INT64_MAX, bk = 0;
-            int ba = 0, bn1 = 0, bn2 = 0, bidx = -1;
-            for (int64_t i = 0; i < m; ++i) {
-                int64_t k; int a, n1, n2, ridx;
-                if (!get(i, k, a, n1, n2, ridx)) continue;
-                if (k <= prevk || k >= bestk) continue;
-                if (c == v || n1 == c || n2 == c) {
-                    bestk = k; bk = k; ba = a; bn1 = n1; bn2 = n2; bidx = ridx;
-                }
-            }
-            if (bestk == INT64_MAX) break;
+        for (int i = 0; i < deg; ++i) {  // ascending k: each incidence contributes at most once
+            int a, n1, n2;
+            get(i, a, n1, n2, nullptr, false);
+            const int rel = c == v ? 0 : (n1 == c ? 1 : (n2 == c ? 2 : -1));
+            if (rel < 0) continue;
             double rv[7];
-            if (bidx >= 0) {
-#pragma unroll
-                for (int j = 0; j < RVALS; ++j) rv[j] = R.vals[j * CAPB + bidx];
-            } else {
-                const double2 own_p = A.q ? A.q[v] : make_double2(0.0, 0.0);
-                const double own_w = A.w ? A.w[v] : 0.0;
-                record_values<KIND>(A, A.T[bk], ba, own_p, own_w, rv);
-            }
-            double d[2], o1[2], o2[2];
-            record_row<KIND>(A, rv, ba, s, d, o1, o2);
-#pragma unroll
-            for (int t = 0; t < NV; ++t) sum[t] = FADD(sum[t], c == v ? d[t] : (bn1 == c ? o1[t] : o2[t]));
-            prevk = bestk;
+            get(i, a, n1, n2, rv, true);
+            for (int t = 0; t < NV; ++t) sum[t] = FADD(sum[t], entry_from<KIND>(A, rv, a, s, rel, t));
         }
-#pragma unroll
         for (int t = 0; t < NV; ++t) {
             if (sum[t] != 0.0) {
                 if (write && out_pos + count < A.capacity) {
@@ -413,285 +585,238 @@ __device__ int64_t general_row(const RowsArgs& A, const BucketRecs& R, bool over
                     A.val[out_pos + count] = sum[t];
                 }
                 ++count;
-            } else if (drops) {
-                ++*drops;
+            } else {
+                ++drops;
             }
         }
         last = c;
     }
-    return count;
+    return RowCount{count, drops};
 }
 
+#ifdef FA_EXP_TIMELINE
+__device__ unsigned long long g_tl[16384 * 6];
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define TL(b, i) do { if (threadIdx.x == 0 && (b) < 16384) g_tl[(b) * 6 + (i)] = gtimer(); } while (0)
+#else
+#define TL(b, i) do { } while (0)
+#endif
+
 template <int KIND>
-__global__ void __launch_bounds__(KindTraits<KIND>::THREADS, 1) k_rows(RowsArgs A) {
+__global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::MIN_BLOCKS)
+    k_rows(const __grid_constant__ RowsArgs A) {
     using TR = KindTraits<KIND>;
-    using SM = RowsSmem<KIND>;
-    constexpr int NV = TR::NV, RPV = TR::RPV, NT = TR::THREADS, STRIDE = TR::STRIDE, CAPR = TR::CAPR;
-    constexpr int RVALS = TR::RVALS;
+    constexpr int NV = TR::NV, RPV = TR::RPV, NT = TR::THREADS, RVALS = TR::RVALS;
     constexpr int NC = 2 * MAXD;
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    // records area
     BucketRecs R;
     R.vals = reinterpret_cast<double*>(smem_raw);
-    R.key = reinterpret_cast<unsigned*>(R.vals + RVALS * CAPB);
-    R.n1 = reinterpret_cast<int*>(R.key + CAPB);
+    R.n1 = reinterpret_cast<int*>(R.vals + RVALS * CAPB);
     R.n2 = R.n1 + CAPB;
-    R.list = reinterpret_cast<unsigned short*>(R.n2 + CAPB);
-    R.vl = reinterpret_cast<unsigned char*>(R.list + CAPB);
-    // staging area (reuses the records area once every row holds its data in registers)
-    double* s_val = reinterpret_cast<double*>(smem_raw);                 // [NT][STRIDE]
-    int32_t* s_col = reinterpret_cast<int32_t*>(s_val + NT * STRIDE);   // [NT][STRIDE]
-    __shared__ int s_cnt[BV];
-    __shared__ int s_start[BV];
-    __shared__ int s_fill[BV];
+    // compact staging of the bucket's CSR segment; reuses the records area once every row
+    // holds its merged entries in registers
+    double* st_val = reinterpret_cast<double*>(smem_raw);
+    int32_t* st_col = reinterpret_cast<int32_t*>(st_val + TR::STAGE);
+    __shared__ unsigned char s_a[CAPB];
+    __shared__ unsigned char s_own[CAPB];
+    R.a = s_a;
+    __shared__ int s_vst[BV + 1];
+    __shared__ double2 s_oq[BV];
+    __shared__ double s_ow[BV];
     __shared__ int64_t s_tile;
     __shared__ uint64_t s_prefix;
     __shared__ int64_t s_warp[NT / 32];
     __shared__ int64_t s_total;
-    __shared__ int64_t s_off[NT + 1];
-    __shared__ unsigned short s_owner[NT * CAPR];
 
     const int tid = threadIdx.x;
     const uint64_t pol_first = l2_evict_first_policy();
     const int64_t b = next_tile(A.ticket, &s_tile);  // bucket, in launch order
-    const unsigned filled = A.bfill[b];
-    const bool overflow = filled > unsigned(CAPB);
-    const int n = overflow ? 0 : int(filled);
-    const int64_t vbase = A.v0 + b * BV;
-    const unsigned* bkeys = A.keys + b * CAPB;
-
-    __shared__ double2 s_oq[BV];
-    __shared__ double s_ow[BV];
+    TL(b, 0);
+    const int64_t nvl = A.v1 - A.v0;
+    const int64_t vb0 = b * BV;  // first vertex of the bucket (row-block local)
+    const int nvb = int(min(int64_t(BV), nvl - vb0));
+    const unsigned gbase = A.ivptr[vb0];
+    for (int i = tid; i <= BV; i += NT) s_vst[i] = int(A.ivptr[vb0 + min(i, nvb)] - gbase);
+    const int64_t vbase = A.v0 + vb0;
     for (int i = tid; i < BV; i += NT) {
-        s_cnt[i] = 0;
-        s_fill[i] = 0;
         const int64_t vv = vbase + i;
         s_oq[i] = (A.q && vv < A.v1) ? A.q[vv] : make_double2(0.0, 0.0);
         s_ow[i] = (KIND == FA_KIND_MASSW && vv < A.v1) ? A.w[vv] : 0.0;
     }
     __syncthreads();
-    // ---- a) per record: its triangle record (one L1 line: a lane pair loads two 32 B records
-    //         cooperatively and swaps halves), neighbour data, its row values -> shared memory.
-    //         AU rounds are issued together so each warp keeps several loads in flight.
+    const bool overflow = s_vst[BV] > CAPB;
+    const int n = overflow ? 0 : s_vst[BV];
+    for (int vl = tid; vl < nvb && !overflow; vl += NT)
+        for (int j = s_vst[vl]; j < s_vst[vl + 1]; ++j) s_own[j] = (unsigned char)vl;
+    __syncthreads();
+
+    // ---- a) per incidence: plan entry (coalesced), gathers from the L2-resident arrays, the
+    //         row of the element matrix -> shared memory
     {
-        constexpr int AU = 6;
-        const int lane = tid & 31, warp = tid >> 5, half = lane & 1, pair = lane >> 1;
-        const uint4* T4 = reinterpret_cast<const uint4*>(A.T);
-        for (int base0 = warp * 32; base0 < n; base0 += NT * AU) {
-            unsigned key[AU];
-            uint4 la[AU], lb[AU];
-            int idx[AU];
-            bool ok[AU];
+        constexpr int AU = 4;
+        const unsigned* gk = A.skey + gbase;
+        const unsigned* g1 = A.sn1 + gbase;
+        const unsigned* g2 = A.sn2 + gbase;
+        for (int i0 = tid; i0 < n; i0 += NT * AU) {
+            unsigned ka[AU], m1[AU], m2[AU];
 #pragma unroll
             for (int u = 0; u < AU; ++u) {
-                const int base = base0 + u * NT;
-                const int iA = base + pair, iB = base + 16 + pair;
-                const bool okA = iA < n, okB = iB < n;
-                const unsigned keyA = okA ? ld_stream_u32(bkeys + iA, pol_first) : 0u;
-                const unsigned keyB = okB ? ld_stream_u32(bkeys + iB, pol_first) : 0u;
-                la[u] = okA ? T4[2 * int64_t(keyA >> 2) + half] : make_uint4(0u, 0u, 0u, 0u);
-                lb[u] = okB ? T4[2 * int64_t(keyB >> 2) + half] : make_uint4(0u, 0u, 0u, 0u);
-                key[u] = half ? keyB : keyA;  // even lane keeps record A, odd lane record B
-                idx[u] = half ? iB : iA;
-                ok[u] = half ? okB : okA;
+                const int i = i0 + u * NT;
+                const bool ok = i < n;
+                ka[u] = ok ? ld_stream_u32(gk + i, pol_first) : 0u;
+                m1[u] = ok ? ld_stream_u32(g1 + i, pol_first) : 0u;
+                m2[u] = ok ? ld_stream_u32(g2 + i, pol_first) : 0u;
             }
-            TriRec t[AU];
+            Gathered g[AU];
+#pragma unroll
+            for (int u = 0; u < AU; ++u)
+                if (i0 + u * NT < n) g[u] = gather_incidence<KIND>(A, ka[u] >> 2, m1[u], m2[u]);
 #pragma unroll
             for (int u = 0; u < AU; ++u) {
-                const uint4 snd = half ? la[u] : lb[u];
-                uint4 rcv;
-                rcv.x = __shfl_xor_sync(0xffffffffu, snd.x, 1);
-                rcv.y = __shfl_xor_sync(0xffffffffu, snd.y, 1);
-                rcv.z = __shfl_xor_sync(0xffffffffu, snd.z, 1);
-                rcv.w = __shfl_xor_sync(0xffffffffu, snd.w, 1);
-                const uint4 lo = half ? rcv : la[u], hi = half ? lb[u] : rcv;
-                t[u].c = make_int4(int(lo.x), int(lo.y), int(lo.z), int(lo.w));
-                t[u].v = make_double2(__hiloint2double(int(hi.y), int(hi.x)), __hiloint2double(int(hi.w), int(hi.z)));
-            }
-#pragma unroll
-            for (int u = 0; u < AU; ++u) {
-                if (!ok[u]) continue;
-                const int i = idx[u];
-                const int a = key[u] & 3;
-                const int vl = int(sel3(a, t[u].c.x, t[u].c.y, t[u].c.z) - vbase);
-                R.key[i] = key[u];
-                R.n1[i] = sel3(a, t[u].c.y, t[u].c.z, t[u].c.x);
-                R.n2[i] = sel3(a, t[u].c.z, t[u].c.x, t[u].c.y);
-                R.vl[i] = (unsigned char)vl;
-                atomicAdd(&s_cnt[vl], 1);
+                const int i = i0 + u * NT;
+                if (i >= n) break;
+                const int a = int(ka[u] & 3u);
+                const int vl = s_own[i];
                 double rv[7];
-#ifdef FA_EXP_NOVALUES
-                for (int j2 = 0; j2 < 7; ++j2) rv[j2] = 1.0 + j2;
-#else
-                record_values<KIND>(A, t[u], a, s_oq[vl], s_ow[vl], rv);
-#endif
+                incidence_values<KIND>(A, ka[u] >> 2, a, g[u], s_oq[vl], s_ow[vl], rv);
 #pragma unroll
-                for (int j2 = 0; j2 < RVALS; ++j2) R.vals[j2 * CAPB + i] = rv[j2];
+                for (int j = 0; j < RVALS; ++j) R.vals[j * CAPB + i] = rv[j];
+                R.n1[i] = int(m1[u]);
+                R.n2[i] = int(m2[u]);
+                s_a[i] = (unsigned char)a;
             }
         }
     }
     __syncthreads();
-#ifdef FA_EXP_STOP_A
-    if (tid == 0 && n == 12345) A.res->reserved[0] = R.key[0];
-    return;
-#endif
-    // ---- b) counting sort by vertex ---------------------------------------------------------
-    {
-        const int c = tid < BV ? s_cnt[tid] : 0;
-        const int64_t ex = block_exclusive_scan<NT>(int64_t(c), s_warp, &s_total);
-        if (tid < BV) s_start[tid] = int(ex);
-    }
-    __syncthreads();
-    for (int i = tid; i < n; i += NT) {
-        const int vl = R.vl[i];
-        R.list[s_start[vl] + atomicAdd(&s_fill[vl], 1)] = (unsigned short)i;
-    }
-    __syncthreads();
+    TL(b, 1);
 
-#ifdef FA_EXP_STOP_B
-    if (tid == 0 && n == 12345) A.res->reserved[0] = R.list[0];
-    return;
-#endif
+    // ---- c) one thread per matrix row --------------------------------------------------------
     const int vloc = tid / RPV, s = tid % RPV;
     const int64_t v = vbase + vloc;
     const bool active = v < A.v1;
     const int64_t r = (b * BV + vloc) * RPV + s;  // local matrix row
-    const int deg = active ? s_cnt[vloc] : 0;
-    const int start = active ? s_start[vloc] : 0;
+    const int start = s_vst[vloc];
+    const int deg = active ? s_vst[vloc + 1] - start : 0;
     const bool slow = active && (deg > MAXD || overflow);
-    const bool any_slow = __syncthreads_or(slow);
+    const bool fast = active && !slow;
+    const unsigned vv = unsigned(v);
+    int64_t count = 0, drops = 0;
 
-    // ---- c) fast rows: records into registers ----------------------------------------------
-    int nb[NC];
-    double ov[NC][NV];
-    double dsum[NV];
+    // merged row kept in registers, indexed by the (unrolled, static) candidate position:
+    // run_val[j][t] is the sum of the column run that ends before sorted candidate j
+    double dsum[NV], run_val[NC + 1][NV];
+    unsigned sk[NC];
+    int diag_at = -1;  // the diagonal is emitted right after run j == diag_at
 #pragma unroll
     for (int t = 0; t < NV; ++t) dsum[t] = 0.0;
-    const bool fast = active && !slow;
     if (fast) {
-        uint64_t sk[MAXD];
 #pragma unroll
         for (int i = 0; i < MAXD; ++i) {
             if (i < deg) {
-                const int ridx = R.list[start + i];
-                sk[i] = (uint64_t(R.key[ridx]) << 16) | uint64_t(ridx);
+                const int slot = start + i;
+#pragma unroll
+                for (int t = 0; t < NV; ++t)
+                    dsum[t] = FADD(dsum[t], record_entry<KIND>(A, R.vals, slot, s_a[slot], s, 0, t));
+                sk[2 * i] = (unsigned(R.n1[slot]) << 4) | unsigned(2 * i);
+                sk[2 * i + 1] = (unsigned(R.n2[slot]) << 4) | unsigned(2 * i + 1);
             } else {
-                sk[i] = ~uint64_t(0);
+                sk[2 * i] = 0xffffffffu;
+                sk[2 * i + 1] = 0xffffffffu;
             }
         }
-        sort8(sk);
+        sort16(sk);
+        // linear pass: ascending columns; each position summed in ascending k (candidate
+        // slot order within a column); the own vertex's diagonal inserted in place
+        unsigned prev = 0xffffffffu;
+        double sum[NV];
 #pragma unroll
-        for (int i = 0; i < MAXD; ++i) {
-            double d[2], o1[2], o2[2];
-            if (i < deg) {
-                const int ridx = int(sk[i] & 0xffff);
-                const int a = int((sk[i] >> 16) & 3);
-                double rv[7];
+        for (int t = 0; t < NV; ++t) sum[t] = 0.0;
 #pragma unroll
-                for (int j = 0; j < RVALS; ++j) rv[j] = R.vals[j * CAPB + ridx];
-                record_row<KIND>(A, rv, a, s, d, o1, o2);
-                nb[2 * i] = R.n1[ridx];
-                nb[2 * i + 1] = R.n2[ridx];
-            } else {
-                nb[2 * i] = INT_MAX;
-                nb[2 * i + 1] = INT_MAX;
+        for (int j = 0; j <= NC; ++j) {
+            const unsigned key = j < NC ? sk[j] : 0xffffffffu;
+            const unsigned c = key == 0xffffffffu ? 0xffffffffu : (key >> 4);
 #pragma unroll
-                for (int t = 0; t < 2; ++t) d[t] = o1[t] = o2[t] = 0.0;
+            for (int t = 0; t < NV; ++t) run_val[j][t] = 0.0;
+            if (c != prev) {
+                if (prev != 0xffffffffu) {
+#pragma unroll
+                    for (int t = 0; t < NV; ++t) {
+                        run_val[j][t] = sum[t];
+                        if (sum[t] != 0.0) ++count; else ++drops;
+                    }
+                }
+                if (diag_at < 0 && vv < c) {
+                    diag_at = j;
+#pragma unroll
+                    for (int t = 0; t < NV; ++t) {
+                        if (dsum[t] != 0.0) ++count; else ++drops;
+                    }
+                }
+#pragma unroll
+                for (int t = 0; t < NV; ++t) sum[t] = 0.0;
+                prev = c;
             }
+            if (j < NC && c != 0xffffffffu) {
+                const int sl = int(key & 15);
+                const int slot = start + (sl >> 1);
 #pragma unroll
-            for (int t = 0; t < NV; ++t) {
-                dsum[t] = FADD(dsum[t], d[t]);
-                ov[2 * i][t] = o1[t];
-                ov[2 * i + 1][t] = o2[t];
+                for (int t = 0; t < NV; ++t)
+                    sum[t] = FADD(sum[t], record_entry<KIND>(A, R.vals, slot, s_a[slot], s, 1 + (sl & 1), t));
             }
-        }
-    } else {
-#pragma unroll
-        for (int j = 0; j < NC; ++j) {
-            nb[j] = INT_MAX;
-#pragma unroll
-            for (int t = 0; t < NV; ++t) ov[j][t] = 0.0;
         }
     }
-    int64_t count = 0, drops = 0;
-    if (slow) count = general_row<KIND>(A, R, overflow, start, deg, v, s, 0, false, &drops);
-    // staging is only used when no row of the bucket needs the records afterwards
-    const bool stage = !any_slow;
-    __syncthreads();  // every row holds its data: the records area becomes the staging area
+    if (slow) {
+        const RowCount rc = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc], s_ow[vloc], s, 0, false);
+        count = rc.count;
+        drops = rc.drops;
+    }
 
-    // merge: vertex columns in ascending order (the row's own vertex included)
-    const int vv = int(v);
-    auto merge = [&](bool to_global, int64_t out_pos) -> int64_t {
-        int last = -1;
-        int64_t cnt = 0;
-        double* my_val = s_val + tid * STRIDE;
-        int32_t* my_col = s_col + tid * STRIDE;
-        while (true) {
-            int c = INT_MAX;
-#pragma unroll
-            for (int j = 0; j < NC; ++j) c = min(c, nb[j] > last ? nb[j] : INT_MAX);
-            const bool diag = vv > last && vv < c;
-            if (diag) c = vv;
-            if (c == INT_MAX) break;
-            double sum[NV];
-#pragma unroll
-            for (int t = 0; t < NV; ++t) sum[t] = diag ? dsum[t] : 0.0;
-            if (!diag) {
-#pragma unroll
-                for (int j = 0; j < NC; ++j)
-                    if (nb[j] == c) {
-#pragma unroll
-                        for (int t = 0; t < NV; ++t) sum[t] = FADD(sum[t], ov[j][t]);
-                    }
-            }
-#pragma unroll
-            for (int t = 0; t < NV; ++t) {
-                if (sum[t] != 0.0) {
-                    const int cc = NV == 1 ? c : 2 * c + t;
-                    if (to_global) {
-                        if (out_pos + cnt < A.capacity) {
-                            A.col[out_pos + cnt] = cc;
-                            A.val[out_pos + cnt] = sum[t];
-                        }
-                    } else if (stage && cnt < CAPR) {
-                        my_col[cnt] = cc;
-                        my_val[cnt] = sum[t];
-                    }
-                    ++cnt;
-                } else if (!to_global) {
-                    ++drops;
-                }
-            }
-            last = c;
-        }
-        return cnt;
-    };
-#ifdef FA_EXP_NOMERGE
-    if (fast) count = deg;
-#else
-    if (fast) count = merge(false, 0);  // writes staging only when `stage` (see below)
-#endif
+    // ---- d) block scan; merged rows into the compact staging; look-back; coalesced copy ---
 #ifdef FA_EXP_STOP_C
     if (count == 12345) A.res->reserved[0] = count;
     return;
 #endif
-    const bool spilled = fast && count > CAPR;
-    const bool direct = __syncthreads_or(spilled) || !stage;
-
-    // ---- d) block scan + look-back: global offset of this bucket's first row -------------
     const int64_t excl = block_exclusive_scan<NT>(count, s_warp, &s_total);
-    s_off[tid] = excl;
-    if (tid == NT - 1) s_off[NT] = excl + count;
-    if (!direct)
-        for (int64_t j = 0; j < count; ++j) s_owner[excl + j] = (unsigned short)tid;  // staged entries' row
-#ifdef FA_EXP_NOLOOKBACK
-    __syncthreads();
-    const uint64_t base = uint64_t(b) * CAPB;
-#else
-    const uint64_t base = lookback_prefix(A.status, b, uint64_t(s_total), &s_prefix);
-#endif
     const int64_t total = s_total;
-
+    TL(b, 2);
+    const bool staged = !__syncthreads_or(slow) && total <= TR::STAGE;  // also: records are dead
+    if (staged && fast) {
+        int64_t o = excl;
+        unsigned prev = 0xffffffffu;
+#pragma unroll
+        for (int j = 0; j <= NC; ++j) {
+            const unsigned key = j < NC ? sk[j] : 0xffffffffu;
+            const unsigned c = key == 0xffffffffu ? 0xffffffffu : (key >> 4);
+            if (c != prev) {
+                if (prev != 0xffffffffu) {
+#pragma unroll
+                    for (int t = 0; t < NV; ++t)
+                        if (run_val[j][t] != 0.0) {
+                            st_col[o] = NV == 1 ? int(prev) : int(2 * prev + t);
+                            st_val[o] = run_val[j][t];
+                            ++o;
+                        }
+                }
+                if (diag_at == j) {
+#pragma unroll
+                    for (int t = 0; t < NV; ++t)
+                        if (dsum[t] != 0.0) {
+                            st_col[o] = NV == 1 ? int(vv) : int(2 * vv + t);
+                            st_val[o] = dsum[t];
+                            ++o;
+                        }
+                }
+                prev = c;
+            }
+        }
+    }
+    TL(b, 3);
+    const uint64_t base = lookback_prefix(A.status, b, uint64_t(total), &s_prefix);  // ends with a barrier
+    TL(b, 4);
     if (active) st_stream_i64(A.rowptr + r, int64_t(base) + excl, pol_first);
     if (active && r == A.nrows - 1) {
         A.rowptr[A.nrows] = int64_t(base) + excl + count;
@@ -699,22 +824,53 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, 1) k_rows(RowsArgs 
     }
     if (drops) atomicAdd(reinterpret_cast<unsigned long long*>(&A.res->dropped), (unsigned long long)drops);
     if (slow) atomicAdd(reinterpret_cast<unsigned long long*>(&A.res->heavy_rows), 1ull);
-
-    if (!direct) {
-        // coalesced copy-out of the staged segment (owner of each entry from s_owner)
+    if (staged) {
         for (int64_t e = tid; e < total; e += NT) {
-            const int lt = s_owner[e];
-            const int j = int(e - s_off[lt]);
             const int64_t g = int64_t(base) + e;
             if (g < A.capacity) {
-                st_stream_i32(A.col + g, s_col[lt * STRIDE + j], pol_first);
-                st_stream_f64(A.val + g, s_val[lt * STRIDE + j], pol_first);
+                st_stream_i32(A.col + g, st_col[e], pol_first);
+                st_stream_f64(A.val + g, st_val[e], pol_first);
             }
         }
     } else {
-        if (fast) merge(true, int64_t(base) + excl);
-        if (slow) general_row<KIND>(A, R, overflow, start, deg, v, s, int64_t(base) + excl, true, nullptr);
+        if (fast) {  // direct writes (normal L2 priority: partial sectors must merge in L2)
+            int64_t o = int64_t(base) + excl;
+            unsigned prev = 0xffffffffu;
+#pragma unroll
+            for (int j = 0; j <= NC; ++j) {
+                const unsigned key = j < NC ? sk[j] : 0xffffffffu;
+                const unsigned c = key == 0xffffffffu ? 0xffffffffu : (key >> 4);
+                if (c != prev) {
+                    if (prev != 0xffffffffu) {
+#pragma unroll
+                        for (int t = 0; t < NV; ++t)
+                            if (run_val[j][t] != 0.0) {
+                                if (o < A.capacity) {
+                                    A.col[o] = NV == 1 ? int(prev) : int(2 * prev + t);
+                                    A.val[o] = run_val[j][t];
+                                }
+                                ++o;
+                            }
+                    }
+                    if (diag_at == j) {
+#pragma unroll
+                        for (int t = 0; t < NV; ++t)
+                            if (dsum[t] != 0.0) {
+                                if (o < A.capacity) {
+                                    A.col[o] = NV == 1 ? int(vv) : int(2 * vv + t);
+                                    A.val[o] = dsum[t];
+                                }
+                                ++o;
+                            }
+                    }
+                    prev = c;
+                }
+            }
+        }
+        if (slow) general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc], s_ow[vloc], s, int64_t(base) + excl, true);
     }
+    __syncthreads();
+    TL(b, 5);
 }
 
 // Optional CUDA events recorded around the row kernel (bench.py's per-kernel roofline).
@@ -722,7 +878,7 @@ static thread_local cudaEvent_t g_timer_begin = nullptr, g_timer_end = nullptr;
 
 template <int KIND>
 static int launch_rows(const RowsArgs& A, int64_t nbuckets, cudaStream_t st) {
-    const size_t smem = RowsSmem<KIND>::bytes;
+    const size_t smem = rows_smem_bytes<KIND>();
     FA_CUDA(cudaFuncSetAttribute(k_rows<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     if (g_timer_begin) FA_CUDA(cudaEventRecord(g_timer_begin, st));
     k_rows<KIND><<<dim3(unsigned(nbuckets)), KindTraits<KIND>::THREADS, smem, st>>>(A);
@@ -738,11 +894,19 @@ static int launch_rows(const RowsArgs& A, int64_t nbuckets, cudaStream_t st) {
 // ------------------------------------------------------------------------------------------
 struct fa_plan {
     int device;
-    int64_t nme, nq, v0, v1, nb, chunk;
-    const int32_t* me;
-    unsigned* bfill;          // nb
-    unsigned* keys;           // nb * CAPB
-    fa::TriRec* T;            // per-triangle records (allocated on first assembly)
+    int64_t nme, nq, v0, v1;
+    int64_t nb;               // row buckets of BV vertices
+    int plog, nparts;
+    int64_t chunk_place;
+    int nblk_place;
+    unsigned* part_off;       // nparts + 1
+    unsigned* part_fill;      // nparts
+    unsigned* M;              // [nblk_place][nparts]
+    uint4* rec;               // 3 * nme (owned incidences, grouped by part)
+    unsigned* skey;           // 3 * nme
+    unsigned* sn1;
+    unsigned* sn2;
+    unsigned* ivptr;          // nv + 1
     uint64_t* status;         // look-back tile status (nb)
     unsigned long long* ticket;
     int64_t ninc;             // -1 until read back
@@ -752,7 +916,17 @@ struct fa_plan {
 using namespace fa;
 
 static void plan_free(fa_plan* p) {
-    cudaFree(p->bfill); cudaFree(p->keys); cudaFree(p->T); cudaFree(p->status); cudaFree(p->ticket);
+    cudaFree(p->part_off); cudaFree(p->part_fill); cudaFree(p->M); cudaFree(p->rec); cudaFree(p->skey); cudaFree(p->sn1);
+    cudaFree(p->sn2); cudaFree(p->ivptr); cudaFree(p->status); cudaFree(p->ticket);
+}
+
+static size_t place_smem_bytes(int nparts) {
+    return size_t(3 * PLACE_TRI) * (sizeof(uint4) + sizeof(unsigned short)) + size_t(3) * sizeof(unsigned) * nparts;
+}
+static size_t sort_smem_bytes(int plog) {
+    const size_t pv = size_t(1) << plog;
+    return sizeof(unsigned) * pv +
+           (pv == (size_t(1) << PLOG0) ? (sizeof(unsigned) * 3 + sizeof(unsigned short)) * SORT_CAP : 0);  // k_part_sort
 }
 
 extern "C" int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t row_begin, int64_t row_end) {
@@ -763,8 +937,9 @@ extern "C" int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t ro
         set_error("row block [%lld, %lld) outside [0, %lld)", (long long)row_begin, (long long)row_end, (long long)nq);
         return FA_ERR_ARGUMENT;
     }
-    if (nme >= (int64_t(1) << 30) || nq >= (int64_t(1) << 30)) {
-        set_error("mesh too large: nme=%lld nq=%lld (limit 2^30 each)", (long long)nme, (long long)nq);
+    if (nme >= (int64_t(1) << 30) || nq >= (int64_t(1) << 28)) {
+        set_error("mesh too large: nme=%lld nq=%lld (limits 2^30 triangles, 2^28 vertices)", (long long)nme,
+                  (long long)nq);
         return FA_ERR_TOO_LARGE;
     }
     fa_plan* p = new (std::nothrow) fa_plan();
@@ -773,17 +948,24 @@ extern "C" int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t ro
     p->nme = nme; p->nq = nq; p->v0 = row_begin; p->v1 = row_end;
     const int64_t nv = row_end - row_begin;
     p->nb = (nv + BV - 1) / BV;
-    // triangles per scatter block: enough that each bucket sees several keys per block,
-    // at most 16384 (u16 shared counters), at least a few blocks per SM
-    int64_t chunk = 2048;
-    while (chunk < 16384 && chunk * 3 < 6 * p->nb && (nme + 2 * chunk - 1) / (2 * chunk) >= 2 * NUM_SMS_B200) chunk *= 2;
-    p->chunk = chunk;
+    p->plog = PLOG0;
+    while (((nv + (int64_t(1) << p->plog) - 1) >> p->plog) > MAX_PARTS) ++p->plog;
+    p->nparts = int((nv + (int64_t(1) << p->plog) - 1) >> p->plog);
+    if (p->nparts < 1) p->nparts = 1;
+    p->chunk_place = (nme + NUM_SMS_B200 - 1) / NUM_SMS_B200;
+    p->nblk_place = int((nme + p->chunk_place - 1) / p->chunk_place);
     p->ninc = -1;
+    const size_t ninc_max = size_t(3) * size_t(nme);
     cudaError_t e = cudaSuccess;
-    const int64_t nbk = p->nb > 0 ? p->nb : 1;
-    if (e == cudaSuccess) e = cudaMalloc(&p->bfill, sizeof(unsigned) * nbk);
-    if (e == cudaSuccess) e = cudaMalloc(&p->keys, sizeof(unsigned) * size_t(nbk) * CAPB);
-    if (e == cudaSuccess) e = cudaMalloc(&p->status, sizeof(uint64_t) * nbk);
+    if (e == cudaSuccess) e = cudaMalloc(&p->part_off, sizeof(unsigned) * (p->nparts + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&p->part_fill, sizeof(unsigned) * p->nparts);
+    if (e == cudaSuccess) e = cudaMalloc(&p->M, sizeof(unsigned) * size_t(p->nblk_place) * p->nparts);
+    if (e == cudaSuccess) e = cudaMalloc(&p->rec, sizeof(uint4) * ninc_max);
+    if (e == cudaSuccess) e = cudaMalloc(&p->skey, sizeof(unsigned) * ninc_max);
+    if (e == cudaSuccess) e = cudaMalloc(&p->sn1, sizeof(unsigned) * ninc_max);
+    if (e == cudaSuccess) e = cudaMalloc(&p->sn2, sizeof(unsigned) * ninc_max);
+    if (e == cudaSuccess) e = cudaMalloc(&p->ivptr, sizeof(unsigned) * (nv + 1));
+    if (e == cudaSuccess) e = cudaMalloc(&p->status, sizeof(uint64_t) * (p->nb > 0 ? p->nb : 1));
     if (e == cudaSuccess) e = cudaMalloc(&p->ticket, sizeof(unsigned long long));
     if (e != cudaSuccess) {
         plan_free(p);
@@ -804,26 +986,39 @@ extern "C" int fa_plan_destroy(fa_plan* p) {
 extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* stream) {
     if (!p || !d_me || !d_res) { set_error("fa_plan_build: NULL argument"); return FA_ERR_ARGUMENT; }
     cudaStream_t st = as_stream(stream);
-    p->me = d_me;
     p->ninc = -1;
     p->built = true;
     k_reset_result<<<1, 32, 0, st>>>(d_res);
     if (p->nb == 0) return FA_OK;
-    FA_CUDA(cudaMemsetAsync(p->bfill, 0, sizeof(unsigned) * p->nb, st));
-    PlanArgs P{d_me, p->nme, p->nq, p->v0, p->v1, p->nb, p->chunk, p->bfill, p->keys, d_res};
-    const unsigned blocks = unsigned((p->nme + p->chunk - 1) / p->chunk);
-    if (p->nb <= SMEM_NB) {
-        const size_t hist_bytes = sizeof(unsigned) * size_t((p->nb + 1) / 2);
-        FA_CUDA(cudaFuncSetAttribute(k_plan_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_bytes)));
-        k_plan_scatter<true><<<blocks, PLAN_BLOCK, hist_bytes, st>>>(P);
-    } else {
-        k_validate_ids<<<grid_for(3 * p->nme, 256), 256, 0, st>>>(d_me, 3 * p->nme, p->nq, d_res);
-        FA_LAUNCH_CHECK("k_validate_ids");
-        k_plan_scatter<false><<<blocks, PLAN_BLOCK, 0, st>>>(P);
-    }
-    FA_LAUNCH_CHECK("k_plan_scatter");
+    PlanArgs P;
+    P.me = d_me; P.nme = p->nme; P.nq = p->nq; P.v0 = p->v0; P.v1 = p->v1;
+    P.plog = p->plog; P.nparts = p->nparts; P.chunk = p->chunk_place;
+    P.part_off = p->part_off; P.part_fill = p->part_fill; P.M = p->M; P.rec = p->rec;
+    P.skey = p->skey; P.sn1 = p->sn1; P.sn2 = p->sn2; P.ivptr = p->ivptr; P.res = d_res;
+    FA_CUDA(cudaMemsetAsync(p->part_off, 0, sizeof(unsigned) * (p->nparts + 1), st));
+    const size_t hist_smem = sizeof(unsigned) * p->nparts;
+    FA_CUDA(cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_smem)));
+    k_part_hist<<<p->nblk_place, PLAN_THREADS, hist_smem, st>>>(P);
+    FA_LAUNCH_CHECK("k_part_hist");
+    k_part_scan<<<1, PLAN_THREADS, 0, st>>>(P);
+    FA_LAUNCH_CHECK("k_part_scan");
+    const size_t place_smem = place_smem_bytes(p->nparts);
+    FA_CUDA(cudaFuncSetAttribute(k_part_place, cudaFuncAttributeMaxDynamicSharedMemorySize, int(place_smem)));
+    k_part_place<<<p->nblk_place, PLAN_THREADS, place_smem, st>>>(P);
+    FA_LAUNCH_CHECK("k_part_place");
+    const size_t sort_smem = sort_smem_bytes(p->plog);
+    FA_CUDA(cudaFuncSetAttribute(k_part_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sort_smem)));
+    k_part_sort<<<p->nparts, SORT_THREADS, sort_smem, st>>>(P);
+    FA_LAUNCH_CHECK("k_part_sort");
     return FA_OK;
 }
+
+#ifdef FA_EXP_TIMELINE
+extern "C" int fa_debug_timeline(void* host_out, int64_t n) {
+    FA_CUDA(cudaMemcpyFromSymbol(host_out, g_tl, sizeof(unsigned long long) * (n < 16384 * 6 ? n : 16384 * 6)));
+    return FA_OK;
+}
+#endif
 
 extern "C" int fa_set_kernel_timer(void* ev_begin, void* ev_end) {
     g_timer_begin = reinterpret_cast<cudaEvent_t>(ev_begin);
@@ -844,15 +1039,9 @@ extern "C" int fa_plan_capacity(fa_plan* p, int kind, int64_t* capacity) {
         if (p->v0 == 0 && p->v1 == p->nq) {
             p->ninc = 3 * p->nme;  // every corner is owned
         } else {
-            // keys written to the row block's buckets (bfill may exceed CAPB: still exact counts)
-            unsigned* h = static_cast<unsigned*>(malloc(sizeof(unsigned) * size_t(p->nb > 0 ? p->nb : 1)));
-            if (!h) { set_error("out of host memory"); return FA_ERR_ARGUMENT; }
-            cudaError_t e = cudaMemcpy(h, p->bfill, sizeof(unsigned) * p->nb, cudaMemcpyDeviceToHost);
-            if (e != cudaSuccess) { free(h); return cuda_status(e, "fa_plan_capacity"); }
-            int64_t s = 0;
-            for (int64_t i = 0; i < p->nb; ++i) s += h[i];
-            free(h);
-            p->ninc = s;
+            unsigned total = 0;
+            FA_CUDA(cudaMemcpy(&total, p->part_off + p->nparts, sizeof(unsigned), cudaMemcpyDeviceToHost));
+            p->ninc = int64_t(total);
         }
     }
     // per vertex: at most 2*deg neighbours + itself; ELASTIC: 2 rows x 2 columns per vertex
@@ -871,7 +1060,6 @@ extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double
         set_error("fa_assemble: vertex coordinates required"); return FA_ERR_ARGUMENT;
     }
     if (kind == FA_KIND_MASSW && !d_w) { set_error("WEIGHTED_MASS requires a WeightField"); return FA_ERR_ARGUMENT; }
-    if (kind == FA_KIND_MASSW && !d_areas) { set_error("WEIGHTED_MASS requires areas"); return FA_ERR_ARGUMENT; }
     cudaStream_t st = as_stream(stream);
     const int64_t nrows = fa_plan_rows(p, kind);
     k_reset_result<<<1, 32, 0, st>>>(d_res);
@@ -879,31 +1067,21 @@ extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double
         FA_CUDA(cudaMemsetAsync(d_rowptr, 0, sizeof(int64_t), st));
         return FA_OK;
     }
-    if (!p->T) FA_CUDA(cudaMalloc(&p->T, sizeof(TriRec) * p->nme));
-    {
-        const int gb = grid_for(p->nme, 256);
-        const double2* q2 = reinterpret_cast<const double2*>(d_q);
-        switch (kind) {
-            case FA_KIND_MASS: k_tri_records<FA_KIND_MASS><<<gb, 256, 0, st>>>(p->me, p->nme, q2, d_areas, p->T, d_res); break;
-            case FA_KIND_MASSW: k_tri_records<FA_KIND_MASSW><<<gb, 256, 0, st>>>(p->me, p->nme, q2, d_areas, p->T, d_res); break;
-            case FA_KIND_STIFF: k_tri_records<FA_KIND_STIFF><<<gb, 256, 0, st>>>(p->me, p->nme, q2, d_areas, p->T, d_res); break;
-            default: k_tri_records<FA_KIND_ELASTIC><<<gb, 256, 0, st>>>(p->me, p->nme, q2, d_areas, p->T, d_res); break;
-        }
-        FA_LAUNCH_CHECK("k_tri_records");
-    }
     FA_CUDA(cudaMemsetAsync(p->status, 0, sizeof(uint64_t) * p->nb, st));
     FA_CUDA(cudaMemsetAsync(p->ticket, 0, sizeof(unsigned long long), st));
     RowsArgs A;
-    A.keys = p->keys; A.bfill = p->bfill; A.me = p->me; A.nme = p->nme;
-    A.q = reinterpret_cast<const double2*>(d_q); A.areas = d_areas; A.w = d_w; A.T = p->T;
+    A.skey = p->skey; A.sn1 = p->sn1; A.sn2 = p->sn2; A.ivptr = p->ivptr;
+    A.q = reinterpret_cast<const double2*>(d_q); A.w = d_w; A.areas = d_areas;
     A.lam = lam; A.mu = mu;
     A.v0 = p->v0; A.v1 = p->v1; A.nrows = nrows;
     A.rowptr = d_rowptr; A.col = d_col; A.val = d_val; A.capacity = capacity;
     A.status = p->status; A.ticket = p->ticket; A.res = d_res;
+    int rc;
     switch (kind) {
-        case FA_KIND_MASS: return launch_rows<FA_KIND_MASS>(A, p->nb, st);
-        case FA_KIND_MASSW: return launch_rows<FA_KIND_MASSW>(A, p->nb, st);
-        case FA_KIND_STIFF: return launch_rows<FA_KIND_STIFF>(A, p->nb, st);
-        default: return launch_rows<FA_KIND_ELASTIC>(A, p->nb, st);
+        case FA_KIND_MASS: rc = launch_rows<FA_KIND_MASS>(A, p->nb, st); break;
+        case FA_KIND_MASSW: rc = launch_rows<FA_KIND_MASSW>(A, p->nb, st); break;
+        case FA_KIND_STIFF: rc = launch_rows<FA_KIND_STIFF>(A, p->nb, st); break;
+        default: rc = launch_rows<FA_KIND_ELASTIC>(A, p->nb, st); break;
     }
+    return rc;
 }

@@ -84,6 +84,13 @@ __device__ __forceinline__ void st_stream_f64(double* p, double v, uint64_t pol)
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
 
+// Drop a dead 128-byte line from L2 without writing it back (its contents become undefined).
+// Used on intermediate plan arrays once consumed, so their dirty lines neither occupy L2
+// nor cost DRAM write bandwidth.
+__device__ __forceinline__ void l2_discard_line(const void* p) {
+    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
+}
+
 template <typename T>
 __device__ __forceinline__ T warp_inclusive_scan(T v) {
     const int lane = threadIdx.x & 31;

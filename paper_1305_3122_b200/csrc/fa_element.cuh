@@ -43,8 +43,12 @@ __device__ __forceinline__ double tri_area(double2 p1, double2 p2, double2 p3) {
 struct MassTri {
     double d, o;  // area/6.0, area/12.0
 };
+// RN(1/6), RN(1/12), RN(1/30) for the constant-divisor division (exact check in ddiv_rcp)
+#define FA_RCP6 0.16666666666666666
+#define FA_RCP12 0.083333333333333329
+#define FA_RCP30 0.033333333333333333
 __device__ __forceinline__ MassTri mass_prepare(double area) {
-    return {FDIV(area, 6.0), FDIV(area, 12.0)};
+    return {ddiv_rcp(area, 6.0, FA_RCP6), ddiv_rcp(area, 12.0, FA_RCP12)};
 }
 __device__ __forceinline__ double mass_entry(const MassTri& t, int a, int b) { return a == b ? t.d : t.o; }
 
@@ -52,9 +56,9 @@ struct MasswTri {
     double e00, e10, e20, e11, e21, e22;  // lower-triangle entries (row il = a + 3b)
 };
 __device__ __forceinline__ MasswTri massw_prepare(double area, double tw0, double tw1, double tw2) {
-    const double W1 = FDIV(FMUL(tw0, area), 30.0);
-    const double W2 = FDIV(FMUL(tw1, area), 30.0);
-    const double W3 = FDIV(FMUL(tw2, area), 30.0);
+    const double W1 = ddiv_rcp(FMUL(tw0, area), 30.0, FA_RCP30);
+    const double W2 = ddiv_rcp(FMUL(tw1, area), 30.0, FA_RCP30);
+    const double W3 = ddiv_rcp(FMUL(tw2, area), 30.0, FA_RCP30);
     MasswTri t;
     t.e00 = FADD(FADD(FMUL(3.0, W1), W2), W3);     // kg[0] = 3*w1 + w2 + w3
     // x / 2.0 == x * 0.5 exactly (division by a power of two is an exact rescale in both)
@@ -64,6 +68,15 @@ __device__ __forceinline__ MasswTri massw_prepare(double area, double tw0, doubl
     t.e21 = FADD(FADD(FMUL(W1, 0.5), W2), W3);     // kg[5] = w1/2 + w2 + w3
     t.e22 = FADD(FADD(W1, W2), FMUL(3.0, W3));     // kg[8] = w1 + w2 + 3*w3
     return t;
+}
+// the six formulas of assembly.py:236-241 from W1..W3
+__device__ __forceinline__ void massw_from_w(double W1, double W2, double W3, MasswTri& t) {
+    t.e00 = FADD(FADD(FMUL(3.0, W1), W2), W3);
+    t.e10 = FADD(FADD(W1, W2), FMUL(W3, 0.5));
+    t.e20 = FADD(FADD(W1, FMUL(W2, 0.5)), W3);
+    t.e11 = FADD(FADD(W1, FMUL(3.0, W2)), W3);
+    t.e21 = FADD(FADD(FMUL(W1, 0.5), W2), W3);
+    t.e22 = FADD(FADD(W1, W2), FMUL(3.0, W3));
 }
 __device__ __forceinline__ double massw_entry(const MasswTri& t, int a, int b) {
     const int hi = a > b ? a : b, lo = a > b ? b : a;

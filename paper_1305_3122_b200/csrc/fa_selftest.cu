@@ -2,6 +2,10 @@
 #include "fa_common.cuh"
 #include "fa_div.cuh"
 
+#define FA_RCP6_ 0.16666666666666666
+#define FA_RCP12_ 0.083333333333333329
+#define FA_RCP30_ 0.033333333333333333
+
 namespace fa {
 
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
@@ -37,6 +41,17 @@ __global__ void k_selftest_div(int64_t n, uint64_t seed, unsigned long long* bad
         if (!both_nan && __double_as_longlong(mine) != __double_as_longlong(ref)) {
             if (atomicAdd(bad, 1ull) == 0) {
                 first[0] = x; first[1] = y; first[2] = mine; first[3] = ref;
+            }
+        }
+        // constant divisors of the mass formulas (x only: y fixed)
+        const double ys[3] = {6.0, 12.0, 30.0}, rs[3] = {FA_RCP6_, FA_RCP12_, FA_RCP30_};
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            const double m2 = ddiv_rcp(x, ys[j], rs[j]), r2 = __ddiv_rn(x, ys[j]);
+            if (!(m2 != m2 && r2 != r2) && __double_as_longlong(m2) != __double_as_longlong(r2)) {
+                if (atomicAdd(bad, 1ull) == 0) {
+                    first[0] = x; first[1] = ys[j]; first[2] = m2; first[3] = r2;
+                }
             }
         }
     }
