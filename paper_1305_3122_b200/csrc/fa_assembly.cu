@@ -437,8 +437,14 @@ __device__ __forceinline__ Gathered gather_incidence(const RowsArgs& A, unsigned
 template <int KIND>
 __device__ __forceinline__ void incidence_values(const RowsArgs& A, unsigned k, int a, const Gathered& g,
                                                  double2 own_p, double own_w, double* out) {
-    const double2 c0 = sel3(a, own_p, g.p2, g.p1), c1 = sel3(a, g.p1, own_p, g.p2), c2 = sel3(a, g.p2, g.p1, own_p);
-    const double ar = A.areas ? g.ar : tri_area(c0, c1, c2);
+    double ar = g.ar;
+    double2 c0, c1, c2;
+    if (KIND == FA_KIND_STIFF || KIND == FA_KIND_ELASTIC || !A.areas) {
+        c0 = sel3(a, own_p, g.p2, g.p1);
+        c1 = sel3(a, g.p1, own_p, g.p2);
+        c2 = sel3(a, g.p2, g.p1, own_p);
+        if (!A.areas) ar = tri_area(c0, c1, c2);
+    }
     if (KIND != FA_KIND_MASSW && ar <= AREA_EPS) atomic_min_i64(&A.res->degenerate_index, int64_t(k));
     if constexpr (KIND == FA_KIND_MASS) {
         const MassTri m = mass_prepare(ar);
@@ -446,11 +452,24 @@ __device__ __forceinline__ void incidence_values(const RowsArgs& A, unsigned k, 
         out[1] = m.o;
         out[2] = m.o;
     } else if constexpr (KIND == FA_KIND_MASSW) {
-        const MasswTri m = massw_prepare(ar, sel3(a, own_w, g.w2, g.w1), sel3(a, g.w1, own_w, g.w2), sel3(a, g.w2, g.w1, own_w));
-        // row a against (a, a+1, a+2): a=0 -> (e00, e10, e20), a=1 -> (e11, e21, e10), a=2 -> (e22, e20, e21)
-        out[0] = sel3(a, m.e00, m.e11, m.e22);
-        out[1] = sel3(a, m.e10, m.e21, m.e20);
-        out[2] = sel3(a, m.e20, m.e10, m.e21);
+        // W of the own corner and of the corners a+1 (n1), a+2 (n2): assembly.py:232-234
+        const double Wo = ddiv_rcp(FMUL(own_w, ar), 30.0, FA_RCP30);
+        const double W1 = ddiv_rcp(FMUL(g.w1, ar), 30.0, FA_RCP30);
+        const double W2 = ddiv_rcp(FMUL(g.w2, ar), 30.0, FA_RCP30);
+        // row a of assembly.py:236-241 in the triangle's corner order (additions are not
+        // associative, so each corner keeps its own formula):
+        //   a=0: diag (3*W0 + W1) + W2,  (0,1) (W0 + W1) + W2/2,  (0,2) (W0 + W1/2) + W2
+        //   a=1: diag (W0 + 3*W1) + W2,  (1,2) (W0/2 + W1) + W2,  (1,0) (W0 + W1) + W2/2
+        //   a=2: diag (W0 + W1) + 3*W2,  (2,0) (W0 + W1/2) + W2,  (2,1) (W0/2 + W1) + W2
+        const double W0t = sel3(a, Wo, W2, W1), W1t = sel3(a, W1, Wo, W2), W2t = sel3(a, W2, W1, Wo);
+        const double t0 = FMUL(3.0, Wo);
+        const double d01 = FADD(W0t, W1t);
+        out[0] = a == 0 ? FADD(FADD(t0, W1t), W2t) : (a == 1 ? FADD(FADD(W0t, t0), W2t) : FADD(d01, t0));
+        const double e10 = FADD(d01, FMUL(W2t, 0.5));                  // (0,1) == (1,0)
+        const double e20 = FADD(FADD(W0t, FMUL(W1t, 0.5)), W2t);       // (0,2) == (2,0)
+        const double e21 = FADD(FADD(FMUL(W0t, 0.5), W1t), W2t);       // (1,2) == (2,1)
+        out[1] = sel3(a, e10, e21, e20);
+        out[2] = sel3(a, e20, e10, e21);
     } else if constexpr (KIND == FA_KIND_STIFF) {
         const int b1 = a == 2 ? 0 : a + 1, b2 = a == 0 ? 2 : a - 1;
         const StiffTri m = stiff_prepare(c0, c1, c2, ar);

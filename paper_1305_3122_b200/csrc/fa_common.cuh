@@ -84,6 +84,25 @@ __device__ __forceinline__ void st_stream_f64(double* p, double v, uint64_t pol)
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
 
+// Randomly gathered arrays (areas, q, w) are pulled into L2 once, sequentially, with an
+// evict-last priority, and gathered with the same priority: every later random access hits L2
+// instead of paying a DRAM round trip per 32-byte sector.
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ld_keep_f64(const double* p, uint64_t pol) {
+    double v;
+    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double2 ld_keep_f64x2(const double2* p, uint64_t pol) {
+    double2 v;
+    asm volatile("ld.global.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;" : "=d"(v.x), "=d"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+
 // Drop a dead 128-byte line from L2 without writing it back (its contents become undefined).
 // Used on intermediate plan arrays once consumed, so their dirty lines neither occupy L2
 // nor cost DRAM write bandwidth.
@@ -152,12 +171,14 @@ __device__ __forceinline__ uint64_t lookback_prefix(uint64_t* status, int64_t ti
             if (lane == 0) st_volatile_u64(&status[tile], lb_pack(1, aggregate));
             uint64_t excl = 0;
             int64_t pred = tile - 1;
+            unsigned backoff = 32;  // ns; doubles while predecessors are still empty (frees issue slots)
             while (true) {
                 int64_t t = pred - lane;
                 uint64_t w = t >= 0 ? ld_volatile_u64(&status[t]) : lb_pack(2, 0);
                 uint64_t flag = w >> 62;
                 if (__any_sync(0xffffffffu, flag == 0)) {
-                    __nanosleep(32);
+                    __nanosleep(backoff);
+                    backoff = backoff < 1024 ? 2 * backoff : 1024;
                     continue;
                 }
                 unsigned pmask = __ballot_sync(0xffffffffu, flag == 2);

@@ -83,31 +83,19 @@ __device__ __forceinline__ double ddiv_slow(double x, double y) {
     return __longlong_as_double(sign | bits);
 }
 
-// x / y for a divisor known in advance with r = RN(1/y) (e.g. the constants 6, 12, 30 of the
-// mass formulas): q = x*r, one residual correction, then the same exact check as ddiv.
+// x / y for a divisor known in advance with r = RN(1/y) (the constants 6, 12, 30 of the mass
+// formulas).  q0 = RN(x r) is within 1.5 ulp of x/y; one correction q1 = RN(q0 + RN(x - y q0) r)
+// (the residual is exact with an fma) makes it faithful; Markstein's theorem (a faithful q and
+// an approximation of 1/y with relative error < 2^-53, which RN(1/y) is, give
+// RN(q + (x - y q) r) = RN(x/y) in the normal range) makes the second correction correctly
+// rounded.  Operands outside the safe exponent range take the exact integer path.
 __device__ __forceinline__ double ddiv_rcp(double x, double y, double r) {
     const uint64_t bx = __double_as_longlong(x);
     const int ex = int((bx >> 52) & 0x7ff) - 1023;
     if (!(ex >= -960 && ex <= 960)) return ddiv_slow(x, y);
-    const uint64_t sign = bx & 0x8000000000000000ull;  // y > 0 here
-    const double ax = fabs(x);
-    double q = __dmul_rn(ax, r);
-    double rem = __fma_rn(-q, y, ax);
-    q = __fma_rn(rem, r, q);
-    rem = __fma_rn(-q, y, ax);
-    const uint64_t bq = __double_as_longlong(q);
-    const uint64_t qexp = bq & 0x7ff0000000000000ull;
-    const double half_up = __longlong_as_double(qexp - (53ull << 52));
-    const bool pow2 = (bq & 0xfffffffffffffull) == 0;
-    const double half_dn = pow2 ? __longlong_as_double(qexp - (54ull << 52)) : half_up;
-    if (rem > 0.0) {
-        const double lim = __dmul_rn(half_up, y);
-        if (rem > lim || (rem == lim && (bq & 1))) q = __longlong_as_double(bq + 1);
-    } else if (rem < 0.0) {
-        const double lim = __dmul_rn(half_dn, y);
-        if (-rem > lim || (-rem == lim && (bq & 1))) q = __longlong_as_double(bq - 1);
-    }
-    return __longlong_as_double(__double_as_longlong(q) | sign);
+    double q = __dmul_rn(x, r);
+    q = __fma_rn(__fma_rn(-q, y, x), r, q);
+    return __fma_rn(__fma_rn(-q, y, x), r, q);
 }
 
 __device__ __forceinline__ double ddiv(double x, double y) {
