@@ -6,9 +6,10 @@ build, plus achieved HBM GB/s.  Workload: BASELINE configs[1] = C2, the P1 weigh
 matrix on the seeded jittered/permuted unit-square mesh with N=1024 (2,097,152 triangles,
 1,050,625 vertices, vertex weights U(0.5, 2)); other configs via --config.
 
-One step = one complete OptV2 assembly from device-resident inputs: plan build (vertex-bucket
-incidence scatter) + per-triangle records + fused row kernel writing rowptr/col/val, i.e. the
-reference's `assemble(mesh, kind, OPTV2)` with nothing cached between steps ("cold").  The L2
+One step = one complete OptV2 assembly from device-resident inputs: plan build (part
+histogram, staged part placement, per-part vertex sort) + fused row kernel writing
+rowptr/col/val, i.e. the reference's `assemble(mesh, kind, OPTV2)` with nothing cached between
+steps ("cold").  The L2
 is flushed (a 512 MB buffer is zeroed) between timed steps, outside the timed windows.
 N > 1 (torchrun): rank g assembles the matrix rows of vertex block g (row-block
 decomposition); the step includes the NCCL allgather of the per-rank nnz
@@ -37,6 +38,9 @@ import numpy as np  # noqa: E402
 
 METRIC = "triangles assembled/sec (device-timed, incl. CSR build)"
 UNIT = "triangles/s"
+# our kernels launched per cold step (fa_plan_build + fa_assemble); memsets are not counted
+LAUNCHES_PER_STEP = ["k_reset_result", "k_part_hist", "k_part_scan", "k_part_place", "k_part_sort",
+                     "k_reset_result", "k_rows"]
 DEFAULT_CONFIG = "C2"
 DESCR = {
     "C1": "P1 mass, N=256 seeded jittered/permuted unit square",
@@ -50,7 +54,7 @@ DESCR = {
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default=DEFAULT_CONFIG)
@@ -88,49 +92,79 @@ def alg_bytes(kind, nme, nq, n_rows, nnz, owned_all=True):
 
 
 class ClockSampler:
-    """nvidia-smi clocks and throttle reasons during the timed region (B200_PROFILING.md)."""
+    """nvidia-smi clocks and throttle reasons during the timed region (B200_PROFILING.md).
+
+    A background thread issues single-shot queries back to back (a looping nvidia-smi writing
+    into a pipe buffers its output and loses it when terminated); every sample is timestamped
+    and the summary keeps the samples taken inside [mark_start, mark_end].  When the timed region
+    is shorter than one query, the samples adjacent to it are reported and flagged."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, gpu_index: int):
+        import threading
+
         self.gpu = gpu_index
-        self.proc = None
+        self.samples = []  # (t_mid, sm, smax, reasons)
+        self.stop_evt = threading.Event()
+        self.thread = threading.Thread(target=self._run, daemon=True)
+        self.t0 = self.t1 = None
+        self.ok = True
 
-    def start(self):
+    def _query(self):
+        t_a = time.perf_counter()
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except (OSError, ValueError):
-            self.proc = None
-
-    def stop(self):
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.proc.terminate()
-        try:
-            out, _ = self.proc.communicate(timeout=5)
-        except subprocess.TimeoutExpired:
-            self.proc.kill()
-            out, _ = self.proc.communicate()
-        sm, smax, reasons = [], [], set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            out = subprocess.run(["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.FIELDS}",
+                                  "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5).stdout
+        except (OSError, subprocess.SubprocessError):
+            self.ok = False
+            return
+        t_b = time.perf_counter()
         for line in out.strip().splitlines():
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 9:
                 continue
             try:
-                sm.append(float(parts[1]))
-                smax.append(float(parts[2]))
+                sm, smax = float(parts[1]), float(parts[2])
             except ValueError:
                 continue
-            for nm, val in zip(names, parts[5:9]):
-                if val.lower() == "active":
-                    reasons.add(nm)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(smax) if smax else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+            reasons = {nm for nm, val in zip(self.NAMES, parts[5:9]) if val.lower() == "active"}
+            self.samples.append(((t_a + t_b) / 2, sm, smax, reasons))
+
+    def _run(self):
+        while not self.stop_evt.is_set() and self.ok:
+            self._query()
+
+    def start(self):
+        self.thread.start()
+        deadline = time.perf_counter() + 10
+        while not self.samples and self.ok and time.perf_counter() < deadline:
+            time.sleep(0.01)
+
+    def mark_start(self):
+        self.t0 = time.perf_counter()
+
+    def mark_end(self):
+        self.t1 = time.perf_counter()
+
+    def stop(self):
+        self.stop_evt.set()
+        self.thread.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        inside = [s for s in self.samples if self.t0 <= s[0] <= self.t1]
+        note = "sampled inside the timed region"
+        if not inside:  # region shorter than a query: the samples just before and after it
+            before = [s for s in self.samples if s[0] < self.t0][-1:]
+            after = [s for s in self.samples if s[0] > self.t1][:1]
+            inside = before + after
+            note = "timed region shorter than one nvidia-smi query: adjacent samples"
+        reasons = set().union(*(s[3] for s in inside)) if inside else set()
+        return {"sm_mhz": statistics.median(s[1] for s in inside), "sm_max_mhz": max(s[2] for s in inside),
+                "reasons": sorted(reasons), "samples": len(inside), "note": note}
 
 
 def measured_peak():
@@ -304,14 +338,16 @@ def run_ours(args):
         step(True)
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
+    clocks.start()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    clocks.mark_start()
     per_step, rows_ms = timed_loop(args.steps, cold=True)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
+    clocks.mark_end()
     clock_info = clocks.stop()
     r = res.fetch()
     local_nnz = int(r.nnz)
@@ -375,7 +411,8 @@ def run_ours(args):
             "data": f"synthetic: seeded jittered/permuted unit-square mesh (SURVEY.md §8(d)), seed {args.seed}",
             "config": {"workload": f"{args.config}: {DESCR[args.config]}", "nq": sm.nq, "nme": sm.nme, "nnz": total_nnz,
                        "seed": args.seed, "parallelism": f"row-blocks x{world}" if world > 1 else "single GPU",
-                       "step": "cold: plan build + records + fused row kernel (+ NCCL nnz allgather when N>1)",
+                       "step": "cold: plan build (part histogram, placement, per-part vertex sort) + fused row "
+                               "kernel (+ NCCL nnz allgather when N>1)",
                        "l2": "512 MB buffer zeroed between timed steps (outside the timed windows)"},
             "hbm_gbs_whole_step": ab_total / (total_ms / args.steps * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "kernel": "k_rows (fused element + sparse() row kernel)",
@@ -384,11 +421,11 @@ def run_ours(args):
                          "peak_source": peak_src},
             "roofline_whole_step_frac": (ab_total / (total_ms / args.steps * 1e-3) / 1e9) / peak,
             "warm": {"value": sm.nme / (warm_ms * 1e-3), "ms_per_step": warm_ms,
-                     "what": "plan reused (symbolic pattern cached): records + row kernel only"},
+                     "what": "plan reused (vertex-sorted incidences cached): row kernel only"},
             "clocks": clock_info,
             "e2e": e2e,
-            "gpu_launches": 5 * args.steps,
-            "gpu_launches_detail": "per step: k_reset_result x2, k_plan_scatter, k_tri_records, k_rows",
+            "gpu_launches": len(LAUNCHES_PER_STEP) * args.steps,
+            "gpu_launches_detail": "per step: " + ", ".join(LAUNCHES_PER_STEP),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
