@@ -41,6 +41,9 @@
 #include "fa_common.cuh"
 #include "fa_element.cuh"
 
+#ifndef FA_ROWS_AU
+#define FA_ROWS_AU 4  // incidences in flight per thread in the row kernel phase a
+#endif
 #ifndef FA_ROWS_MINB
 #define FA_ROWS_MINB 4  // scalar kinds: <= 128 registers, no local memory
 #endif
@@ -56,6 +59,24 @@ constexpr int PLAN_THREADS = 1024;
 constexpr int SORT_THREADS = 512;   // k_part_sort (2 blocks / SM, 64 registers)
 constexpr int PLACE_TRI = 2048;    // triangles per placement round
 constexpr int SORT_CAP = 7680;     // part incidences sorted in shared memory (2 blocks / SM)
+
+// Resets the result block and zeroes the counters the following kernels accumulate into
+// (grid-stride; replaces separate memsets).
+__global__ void k_reset(fa_result* r, unsigned* z32, int64_t n32, uint64_t* z64, int64_t n64) {
+    const int64_t stride = int64_t(gridDim.x) * blockDim.x;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n32; i += stride) z32[i] = 0;
+    for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n64; i += stride) z64[i] = 0;
+    if (threadIdx.x == 0 && blockIdx.x == 0) {
+        r->nnz = 0;
+        r->degenerate_index = INT64_MAX;
+        r->index_error_pos = INT64_MAX;
+        r->col_error_pos = INT64_MAX;
+        r->dropped = 0;
+        r->heavy_rows = 0;
+        r->reserved[0] = 0;
+        r->reserved[1] = 0;
+    }
+}
 
 __global__ void k_reset_result(fa_result* r) {
     if (threadIdx.x == 0 && blockIdx.x == 0) {
@@ -387,6 +408,10 @@ struct RowsArgs {
     int64_t capacity;
     uint64_t* status;
     unsigned long long* ticket;
+    unsigned long long* bsym;  // per bucket: symbolic start of its CSR segment
+    unsigned* blen;         // per bucket: symbolic length
+    unsigned* bdrop;        // per bucket: entries that summed to exactly zero
+    unsigned* read_done;    // per bucket: k_compact flag, zeroed here
     fa_result* res;
 };
 
@@ -399,7 +424,7 @@ struct KindTraits {
     // triangle's gradients + area (entries are formed per dof row in the merge)
     static constexpr int RVALS = KIND == FA_KIND_ELASTIC ? 7 : 3;
     static constexpr int MIN_BLOCKS = KIND == FA_KIND_ELASTIC ? 2 : FA_ROWS_MINB;
-    static constexpr size_t REC_BYTES = size_t(CAPB) * (RVALS * 8 + 8);
+    static constexpr size_t REC_BYTES = size_t(CAPB) * (RVALS * 8 + 12);
     static constexpr int STAGE = int(REC_BYTES / 12);  // staged entries fitting the records area
 };
 
@@ -539,27 +564,28 @@ struct BucketRecs {
     double* vals;          // [RVALS][CAPB]
     int* n1;               // [CAPB]
     int* n2;               // [CAPB]
-    unsigned char* a;      // [CAPB] local corner of the row's vertex
+    unsigned* ka;          // [CAPB] k << 2 | local corner of the row's vertex
 };
 
 struct RowCount {
-    int64_t count, drops;
+    int64_t count, zeros;
 };
 
-// General path for one row: O(d^2) selection with the same summation order (ascending k per
-// position).  Incidences from shared memory (slots start..start+deg, ascending k) or, when the
-// bucket did not fit (overflow), from the plan in global memory (positions gfirst.., same
-// order) with the values recomputed.  Writes when `write`.
+// General path for one row: O(d^2) selection of the columns in ascending order.  `values`
+// false: the symbolic entry count only.  `values` true: each position summed in ascending k
+// (incidences from shared memory, slots start.., or - overflowing bucket - from the plan in
+// global memory with the values recomputed); entries written at out_pos.. when `write`, exact
+// zeros kept (removed later by k_compact) or dropped per `keep_zeros`; zero sums counted.
 template <int KIND>
 __device__ __noinline__ RowCount general_row(const RowsArgs& A, BucketRecs R, bool overflow, int64_t gfirst, int start,
                                              int deg, int64_t v, double2 own_p, double own_w, int s, int64_t out_pos,
-                                             bool write) {
+                                             bool values, bool write = true, bool keep_zeros = true) {
     constexpr int NV = KindTraits<KIND>::NV;
     constexpr int RVALS = KindTraits<KIND>::RVALS;
     auto get = [&](int i, int& a, int& n1, int& n2, double* rv, bool need_vals) {
         if (!overflow) {
             const int slot = start + i;
-            a = R.a[slot];
+            a = int(R.ka[slot] & 3u);
             n1 = R.n1[slot];
             n2 = R.n2[slot];
             if (need_vals)
@@ -575,7 +601,7 @@ __device__ __noinline__ RowCount general_row(const RowsArgs& A, BucketRecs R, bo
             incidence_values<KIND>(A, ka >> 2, a, g, own_p, own_w, rv);
         }
     };
-    int64_t last = -1, count = 0, drops = 0;
+    int64_t last = -1, count = 0, zeros = 0;
     while (true) {
         int64_t c = INT64_MAX;  // next vertex column
         if (v > last) c = v;
@@ -586,31 +612,34 @@ __device__ __noinline__ RowCount general_row(const RowsArgs& A, BucketRecs R, bo
             if (n2 > last && n2 < c) c = n2;
         }
         if (c == INT64_MAX) break;
-        double sum[NV];
-        for (int t = 0; t < NV; ++t) sum[t] = 0.0;
-        for (int i = 0; i < deg; ++i) {  // ascending k: each incidence contributes at most once
-            int a, n1, n2;
-            get(i, a, n1, n2, nullptr, false);
-            const int rel = c == v ? 0 : (n1 == c ? 1 : (n2 == c ? 2 : -1));
-            if (rel < 0) continue;
-            double rv[7];
-            get(i, a, n1, n2, rv, true);
-            for (int t = 0; t < NV; ++t) sum[t] = FADD(sum[t], entry_from<KIND>(A, rv, a, s, rel, t));
-        }
-        for (int t = 0; t < NV; ++t) {
-            if (sum[t] != 0.0) {
+        if (values) {
+            double sum[NV];
+            for (int t = 0; t < NV; ++t) sum[t] = 0.0;
+            for (int i = 0; i < deg; ++i) {  // ascending k: each incidence contributes at most once
+                int a, n1, n2;
+                get(i, a, n1, n2, nullptr, false);
+                const int rel = c == v ? 0 : (n1 == c ? 1 : (n2 == c ? 2 : -1));
+                if (rel < 0) continue;
+                double rv[7];
+                get(i, a, n1, n2, rv, true);
+                for (int t = 0; t < NV; ++t) sum[t] = FADD(sum[t], entry_from<KIND>(A, rv, a, s, rel, t));
+            }
+            for (int t = 0; t < NV; ++t) {
+                const bool z = sum[t] == 0.0;
+                if (z) ++zeros;
+                if (z && !keep_zeros) continue;
                 if (write && out_pos + count < A.capacity) {
                     A.col[out_pos + count] = int32_t(NV == 1 ? c : 2 * c + t);
                     A.val[out_pos + count] = sum[t];
                 }
                 ++count;
-            } else {
-                ++drops;
             }
+        } else {
+            count += NV;
         }
         last = c;
     }
-    return RowCount{count, drops};
+    return RowCount{count, zeros};
 }
 
 #ifdef FA_EXP_TIMELINE
@@ -625,6 +654,18 @@ __device__ __forceinline__ unsigned long long gtimer() {
 #define TL(b, i) do { } while (0)
 #endif
 
+// Sorted candidate columns of a fast row: (neighbour << 4 | slot), slot = 2 * incidence +
+// (0: n1, 1: n2), unused keys 0xffffffff.
+__device__ __forceinline__ void row_keys(const BucketRecs& R, int start, int deg, unsigned (&sk)[2 * MAXD]) {
+#pragma unroll
+    for (int i = 0; i < MAXD; ++i) {
+        const bool ok = i < deg;
+        sk[2 * i] = ok ? (unsigned(R.n1[start + i]) << 4) | unsigned(2 * i) : 0xffffffffu;
+        sk[2 * i + 1] = ok ? (unsigned(R.n2[start + i]) << 4) | unsigned(2 * i + 1) : 0xffffffffu;
+    }
+    sort16(sk);
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::MIN_BLOCKS)
     k_rows(const __grid_constant__ RowsArgs A) {
@@ -636,13 +677,12 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     R.vals = reinterpret_cast<double*>(smem_raw);
     R.n1 = reinterpret_cast<int*>(R.vals + RVALS * CAPB);
     R.n2 = R.n1 + CAPB;
+    R.ka = reinterpret_cast<unsigned*>(R.n2 + CAPB);
     // compact staging of the bucket's CSR segment; reuses the records area once every row
     // holds its merged entries in registers
     double* st_val = reinterpret_cast<double*>(smem_raw);
     int32_t* st_col = reinterpret_cast<int32_t*>(st_val + TR::STAGE);
-    __shared__ unsigned char s_a[CAPB];
     __shared__ unsigned char s_own[CAPB];
-    R.a = s_a;
     __shared__ int s_vst[BV + 1];
     __shared__ double2 s_oq[BV];
     __shared__ double s_ow[BV];
@@ -671,49 +711,15 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     const int n = overflow ? 0 : s_vst[BV];
     for (int vl = tid; vl < nvb && !overflow; vl += NT)
         for (int j = s_vst[vl]; j < s_vst[vl + 1]; ++j) s_own[j] = (unsigned char)vl;
-    __syncthreads();
-
-    // ---- a) per incidence: plan entry (coalesced), gathers from the L2-resident arrays, the
-    //         row of the element matrix -> shared memory
-    {
-        constexpr int AU = 4;
-        const unsigned* gk = A.skey + gbase;
-        const unsigned* g1 = A.sn1 + gbase;
-        const unsigned* g2 = A.sn2 + gbase;
-        for (int i0 = tid; i0 < n; i0 += NT * AU) {
-            unsigned ka[AU], m1[AU], m2[AU];
-#pragma unroll
-            for (int u = 0; u < AU; ++u) {
-                const int i = i0 + u * NT;
-                const bool ok = i < n;
-                ka[u] = ok ? ld_stream_u32(gk + i, pol_first) : 0u;
-                m1[u] = ok ? ld_stream_u32(g1 + i, pol_first) : 0u;
-                m2[u] = ok ? ld_stream_u32(g2 + i, pol_first) : 0u;
-            }
-            Gathered g[AU];
-#pragma unroll
-            for (int u = 0; u < AU; ++u)
-                if (i0 + u * NT < n) g[u] = gather_incidence<KIND>(A, ka[u] >> 2, m1[u], m2[u]);
-#pragma unroll
-            for (int u = 0; u < AU; ++u) {
-                const int i = i0 + u * NT;
-                if (i >= n) break;
-                const int a = int(ka[u] & 3u);
-                const int vl = s_own[i];
-                double rv[7];
-                incidence_values<KIND>(A, ka[u] >> 2, a, g[u], s_oq[vl], s_ow[vl], rv);
-#pragma unroll
-                for (int j = 0; j < RVALS; ++j) R.vals[j * CAPB + i] = rv[j];
-                R.n1[i] = int(m1[u]);
-                R.n2[i] = int(m2[u]);
-                s_a[i] = (unsigned char)a;
-            }
-        }
+    // ---- s) the bucket's plan entries -> shared memory (coalesced)
+    for (int i = tid; i < n; i += NT) {
+        R.ka[i] = ld_stream_u32(A.skey + gbase + i, pol_first);
+        R.n1[i] = int(ld_stream_u32(A.sn1 + gbase + i, pol_first));
+        R.n2[i] = int(ld_stream_u32(A.sn2 + gbase + i, pol_first));
     }
     __syncthreads();
-    TL(b, 1);
 
-    // ---- c) one thread per matrix row --------------------------------------------------------
+    // one thread per matrix row
     const int vloc = tid / RPV, s = tid % RPV;
     const int64_t v = vbase + vloc;
     const bool active = v < A.v1;
@@ -723,10 +729,68 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     const bool slow = active && (deg > MAXD || overflow);
     const bool fast = active && !slow;
     const unsigned vv = unsigned(v);
-    int64_t count = 0, drops = 0;
+    // EARLY (scalar kinds): the bucket's symbolic size is published before the numeric work and
+    // exact-zero sums stay as entries for k_compact (they are rare).  Elasticity cancels often,
+    // so it publishes the exact count after the sums instead.
+    constexpr bool EARLY = KIND != FA_KIND_ELASTIC;
+    //    symbolic entry count of the row (unique columns + diagonal); the bucket aggregate is
+    //    published now, before the numeric work, so successors' look-backs find it and this
+    //    bucket's own look-back (after phase c) finds its predecessors' - nobody waits on the
+    //    slow gathers of another bucket
+    int64_t count = 0, excl = 0, total = 0;
+    if (EARLY && fast) {
+        unsigned sk[NC];
+        row_keys(R, start, deg, sk);
+        unsigned prev = 0xffffffffu, distinct = 0;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+            const unsigned c = sk[j] == 0xffffffffu ? 0xffffffffu : (sk[j] >> 4);
+            if (c != 0xffffffffu && c != prev) ++distinct;
+            prev = c;
+        }
+        count = int64_t(NV) * (distinct + 1);
+    }
+    if (EARLY && slow)
+        count = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc], s_ow[vloc], s, 0,
+                                  false).count;
+    if (EARLY) {
+        excl = block_exclusive_scan<NT>(count, s_warp, &s_total);
+        total = s_total;
+        lookback_publish(A.status, b, uint64_t(total));
+    }
+    TL(b, 1);
 
-    // merged row kept in registers, indexed by the (unrolled, static) candidate position:
-    // run_val[j][t] is the sum of the column run that ends before sorted candidate j
+    // ---- a) per incidence (balanced over threads): gathers from the L2-resident arrays, the
+    //         row of the element matrix -> shared memory
+    {
+        constexpr int AU = FA_ROWS_AU;
+        for (int i0 = tid; i0 < n; i0 += NT * AU) {
+            unsigned ka[AU];
+            Gathered g[AU];
+#pragma unroll
+            for (int u = 0; u < AU; ++u) {
+                const int i = i0 + u * NT;
+                ka[u] = i < n ? R.ka[i] : 0u;
+                if (i < n) g[u] = gather_incidence<KIND>(A, ka[u] >> 2, unsigned(R.n1[i]), unsigned(R.n2[i]));
+            }
+#pragma unroll
+            for (int u = 0; u < AU; ++u) {
+                const int i = i0 + u * NT;
+                if (i >= n) break;
+                const int vl = s_own[i];
+                double rv[7];
+                incidence_values<KIND>(A, ka[u] >> 2, int(ka[u] & 3u), g[u], s_oq[vl], s_ow[vl], rv);
+#pragma unroll
+                for (int j = 0; j < RVALS; ++j) R.vals[j * CAPB + i] = rv[j];
+            }
+        }
+    }
+    __syncthreads();
+    TL(b, 2);
+
+    // ---- c) per row: each position summed sequentially in ascending k (== stable argsort +
+    //         bincount of the reference); exact-zero sums stay as entries and are counted
+    int64_t zeros = 0;
     double dsum[NV], run_val[NC + 1][NV];
     unsigned sk[NC];
     int diag_at = -1;  // the diagonal is emitted right after run j == diag_at
@@ -739,17 +803,10 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
                 const int slot = start + i;
 #pragma unroll
                 for (int t = 0; t < NV; ++t)
-                    dsum[t] = FADD(dsum[t], record_entry<KIND>(A, R.vals, slot, s_a[slot], s, 0, t));
-                sk[2 * i] = (unsigned(R.n1[slot]) << 4) | unsigned(2 * i);
-                sk[2 * i + 1] = (unsigned(R.n2[slot]) << 4) | unsigned(2 * i + 1);
-            } else {
-                sk[2 * i] = 0xffffffffu;
-                sk[2 * i + 1] = 0xffffffffu;
+                    dsum[t] = FADD(dsum[t], record_entry<KIND>(A, R.vals, slot, int(R.ka[slot] & 3u), s, 0, t));
             }
         }
-        sort16(sk);
-        // linear pass: ascending columns; each position summed in ascending k (candidate
-        // slot order within a column); the own vertex's diagonal inserted in place
+        row_keys(R, start, deg, sk);
         unsigned prev = 0xffffffffu;
         double sum[NV];
 #pragma unroll
@@ -765,14 +822,16 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
 #pragma unroll
                     for (int t = 0; t < NV; ++t) {
                         run_val[j][t] = sum[t];
-                        if (sum[t] != 0.0) ++count; else ++drops;
+                        if (sum[t] == 0.0) ++zeros;
+                        else if (!EARLY) ++count;
                     }
                 }
                 if (diag_at < 0 && vv < c) {
                     diag_at = j;
 #pragma unroll
                     for (int t = 0; t < NV; ++t) {
-                        if (dsum[t] != 0.0) ++count; else ++drops;
+                        if (dsum[t] == 0.0) ++zeros;
+                        else if (!EARLY) ++count;
                     }
                 }
 #pragma unroll
@@ -784,25 +843,25 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
                 const int slot = start + (sl >> 1);
 #pragma unroll
                 for (int t = 0; t < NV; ++t)
-                    sum[t] = FADD(sum[t], record_entry<KIND>(A, R.vals, slot, s_a[slot], s, 1 + (sl & 1), t));
+                    sum[t] = FADD(sum[t], record_entry<KIND>(A, R.vals, slot, int(R.ka[slot] & 3u), s, 1 + (sl & 1), t));
             }
         }
     }
-    if (slow) {
-        const RowCount rc = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc], s_ow[vloc], s, 0, false);
-        count = rc.count;
-        drops = rc.drops;
+    if (!EARLY) {
+        if (slow) {
+            const RowCount rc = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc],
+                                                  s_ow[vloc], s, 0, true, false, false);
+            count = rc.count;
+            zeros = rc.zeros;
+        }
+        excl = block_exclusive_scan<NT>(count, s_warp, &s_total);
+        total = s_total;
+        lookback_publish(A.status, b, uint64_t(total));
     }
-
-    // ---- d) block scan; merged rows into the compact staging; look-back; coalesced copy ---
-#ifdef FA_EXP_STOP_C
-    if (count == 12345) A.res->reserved[0] = count;
-    return;
-#endif
-    const int64_t excl = block_exclusive_scan<NT>(count, s_warp, &s_total);
-    const int64_t total = s_total;
-    TL(b, 2);
-    const bool staged = !__syncthreads_or(slow) && total <= TR::STAGE;  // also: records are dead
+    TL(b, 3);
+    // ---- d) merged rows into the compact staging (records are dead), look-back (normally
+    //         already resolved), coalesced copy at the symbolic offset
+    const bool staged = !__syncthreads_or(slow) && total <= TR::STAGE;
     if (staged && fast) {
         int64_t o = excl;
         unsigned prev = 0xffffffffu;
@@ -813,35 +872,33 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
             if (c != prev) {
                 if (prev != 0xffffffffu) {
 #pragma unroll
-                    for (int t = 0; t < NV; ++t)
-                        if (run_val[j][t] != 0.0) {
-                            st_col[o] = NV == 1 ? int(prev) : int(2 * prev + t);
-                            st_val[o] = run_val[j][t];
-                            ++o;
-                        }
+                    for (int t = 0; t < NV; ++t) {
+                        if (!EARLY && run_val[j][t] == 0.0) continue;
+                        st_col[o] = NV == 1 ? int(prev) : int(2 * prev + t);
+                        st_val[o] = run_val[j][t];
+                        ++o;
+                    }
                 }
                 if (diag_at == j) {
 #pragma unroll
-                    for (int t = 0; t < NV; ++t)
-                        if (dsum[t] != 0.0) {
-                            st_col[o] = NV == 1 ? int(vv) : int(2 * vv + t);
-                            st_val[o] = dsum[t];
-                            ++o;
-                        }
+                    for (int t = 0; t < NV; ++t) {
+                        if (!EARLY && dsum[t] == 0.0) continue;
+                        st_col[o] = NV == 1 ? int(vv) : int(2 * vv + t);
+                        st_val[o] = dsum[t];
+                        ++o;
+                    }
                 }
                 prev = c;
             }
         }
     }
-    TL(b, 3);
-    const uint64_t base = lookback_prefix(A.status, b, uint64_t(total), &s_prefix);  // ends with a barrier
+    const uint64_t base = lookback_wait(A.status, b, uint64_t(total), &s_prefix);  // ends with a barrier
     TL(b, 4);
     if (active) st_stream_i64(A.rowptr + r, int64_t(base) + excl, pol_first);
     if (active && r == A.nrows - 1) {
         A.rowptr[A.nrows] = int64_t(base) + excl + count;
         A.res->nnz = int64_t(base) + excl + count;
     }
-    if (drops) atomicAdd(reinterpret_cast<unsigned long long*>(&A.res->dropped), (unsigned long long)drops);
     if (slow) atomicAdd(reinterpret_cast<unsigned long long*>(&A.res->heavy_rows), 1ull);
     if (staged) {
         for (int64_t e = tid; e < total; e += NT) {
@@ -862,35 +919,197 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
                 if (c != prev) {
                     if (prev != 0xffffffffu) {
 #pragma unroll
-                        for (int t = 0; t < NV; ++t)
-                            if (run_val[j][t] != 0.0) {
-                                if (o < A.capacity) {
-                                    A.col[o] = NV == 1 ? int(prev) : int(2 * prev + t);
-                                    A.val[o] = run_val[j][t];
-                                }
-                                ++o;
+                        for (int t = 0; t < NV; ++t) {
+                            if (!EARLY && run_val[j][t] == 0.0) continue;
+                            if (o < A.capacity) {
+                                A.col[o] = NV == 1 ? int(prev) : int(2 * prev + t);
+                                A.val[o] = run_val[j][t];
                             }
+                            ++o;
+                        }
                     }
                     if (diag_at == j) {
 #pragma unroll
-                        for (int t = 0; t < NV; ++t)
-                            if (dsum[t] != 0.0) {
-                                if (o < A.capacity) {
-                                    A.col[o] = NV == 1 ? int(vv) : int(2 * vv + t);
-                                    A.val[o] = dsum[t];
-                                }
-                                ++o;
+                        for (int t = 0; t < NV; ++t) {
+                            if (!EARLY && dsum[t] == 0.0) continue;
+                            if (o < A.capacity) {
+                                A.col[o] = NV == 1 ? int(vv) : int(2 * vv + t);
+                                A.val[o] = dsum[t];
                             }
+                            ++o;
+                        }
                     }
                     prev = c;
                 }
             }
         }
-        if (slow) general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc], s_ow[vloc], s, int64_t(base) + excl, true);
+        if (slow) {
+            const RowCount rc = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc],
+                                                  s_ow[vloc], s, int64_t(base) + excl, true, true, EARLY);
+            if (EARLY) zeros = rc.zeros;
+        }
     }
-    __syncthreads();
+    // zero sums of the bucket -> compaction data (k_compact runs only when some exist)
+    block_exclusive_scan<NT>(zeros, s_warp, &s_total);
+    const unsigned bz = unsigned(s_total);
+    if (tid == 0) {
+        A.bsym[b] = base;
+        A.blen[b] = unsigned(total);
+        A.bdrop[b] = EARLY ? bz : 0u;  // !EARLY: already dropped in place
+        A.read_done[b] = 0;
+        if (bz) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(&A.res->dropped), (unsigned long long)bz);
+            if (EARLY) atomicAdd(reinterpret_cast<unsigned long long*>(&A.res->reserved[0]), (unsigned long long)bz);
+        }
+    }
     TL(b, 5);
 }
+
+// Removes the exactly-zero sums (sparse.py:177-179) in place; exits at once when there are
+// none.  Block 0 first scans the per-bucket zero counts (bshift[b] = zeros of all earlier
+// buckets) and fixes nnz; bucket segments then move left by their shift; a bucket writes only
+// after every earlier bucket whose source range overlaps its destination has read its source
+// (ticket order guarantees those are resident or finished).  Persistent grid, all resident.
+constexpr int CMP_THREADS = 256;
+constexpr int CMP_CAP = 4096;  // entries held per bucket (dynamic shared memory)
+__global__ void __launch_bounds__(CMP_THREADS) k_compact(const unsigned long long* __restrict__ bsym,
+                                                          const unsigned* __restrict__ blen,
+                                                          const unsigned* __restrict__ bdrop,
+                                                          const unsigned long long* bshift,
+                                                          unsigned* read_done, unsigned long long* ticket, int64_t nb,
+                                                          int64_t rows_per_bucket, int64_t nrows,
+                                                          int64_t* __restrict__ rowptr, int32_t* col, double* val,
+                                                          fa_result* res, unsigned* scan_ready) {
+    extern __shared__ __align__(16) unsigned char cmp_raw[];
+    double* s_v = reinterpret_cast<double*>(cmp_raw);            // [CMP_CAP]
+    int32_t* s_c = reinterpret_cast<int32_t*>(s_v + CMP_CAP);     // [CMP_CAP]
+    __shared__ unsigned s_warp[CMP_THREADS / 32];
+    __shared__ unsigned s_total;
+    __shared__ int64_t s_tile;
+    const unsigned long long dropped = res->reserved[0];  // exact zeros left in place by k_rows
+    if (dropped == 0) return;
+    const int tid = threadIdx.x;
+    if (blockIdx.x == 0) {
+        __shared__ unsigned long long s_w64[CMP_THREADS / 32];
+        __shared__ unsigned long long s_t64;
+        const int64_t per = (nb + CMP_THREADS - 1) / CMP_THREADS;
+        const int64_t b0 = tid * per, b1 = min(nb, b0 + per);
+        unsigned long long run = 0;
+        for (int64_t i = b0; i < b1; ++i) run += bdrop[i];
+        unsigned long long ex = block_exclusive_scan<CMP_THREADS>(run, s_w64, &s_t64);
+        for (int64_t i = b0; i < b1; ++i) {
+            const_cast<unsigned long long*>(bshift)[i] = ex;
+            ex += bdrop[i];
+        }
+        __syncthreads();
+        if (tid == 0) {
+            const int64_t nnz = rowptr[nrows] - int64_t(dropped);
+            rowptr[nrows] = nnz;
+            res->nnz = nnz;
+            __threadfence();
+            atomicExch(scan_ready, 1u);
+        }
+    }
+    if (tid == 0)
+        while (atomicAdd(scan_ready, 0u) == 0u) __nanosleep(256);
+    __syncthreads();
+    __threadfence();
+    while (true) {  // persistent: buckets in ticket order
+    const int64_t b = next_tile(ticket, &s_tile);
+    if (b >= nb) return;
+    const unsigned long long S = bsym[b], len = blen[b], shift = bshift[b];
+    const unsigned drops = bdrop[b];
+    if (shift == 0 && drops == 0) {
+        if (tid == 0) atomicExch(&read_done[b], 1u);
+        continue;
+    }
+    const unsigned long long D = S - shift;
+    // rows of the bucket: symbolic starts -> compacted starts
+    const int64_t r0 = b * rows_per_bucket, r1 = min(nrows, r0 + rows_per_bucket);
+    // (1) read the segment (whole when it fits) and the symbolic row starts
+    const bool fits = len <= (unsigned long long)CMP_CAP;
+    if (fits) {
+        for (unsigned e = tid; e < len; e += CMP_THREADS) {
+            s_c[e] = col[S + e];
+            s_v[e] = val[S + e];
+        }
+    }
+    int64_t rs = 0, re = 0;
+    const int64_t r = r0 + tid;
+    if (r < r1) {
+        rs = rowptr[r];
+        re = (r + 1 < r1) ? rowptr[r + 1] : int64_t(S + len);
+    }
+    __syncthreads();
+    if (fits && tid == 0) {
+        __threadfence();
+        atomicExch(&read_done[b], 1u);
+    }
+    // (2) wait for earlier buckets whose source overlaps the destination
+    if (tid == 0) {
+        for (int64_t bp = b - 1; bp >= 0; --bp) {
+            if (bsym[bp] + blen[bp] <= D) break;
+            while (atomicAdd(&read_done[bp], 0u) == 0u) __nanosleep(64);
+        }
+        __threadfence();
+    }
+    __syncthreads();
+    // (3) compacted row starts
+    unsigned kept = 0;
+    if (r < r1) {
+        for (int64_t e = rs; e < re; ++e) {
+            const double x = fits ? s_v[e - int64_t(S)] : val[e];
+            kept += x != 0.0 ? 1u : 0u;
+        }
+    }
+    const unsigned kex = block_exclusive_scan<CMP_THREADS>(kept, s_warp, &s_total);
+    if (r < r1) rowptr[r] = int64_t(D) + kex;
+    // (4) entries
+    if (fits) {
+        unsigned base = 0;
+        for (unsigned c0 = 0; c0 < len; c0 += CMP_THREADS) {
+            const unsigned e = c0 + tid;
+            const bool keep = e < len && s_v[e] != 0.0;
+            const unsigned rank = block_exclusive_scan<CMP_THREADS>(keep ? 1u : 0u, s_warp, &s_total);
+            if (keep) {
+                col[D + base + rank] = s_c[e];
+                val[D + base + rank] = s_v[e];
+            }
+            base += s_total;
+            __syncthreads();
+        }
+    } else {
+        // large segment: chunk by chunk (each chunk read before it is written; destinations
+        // never reach past the chunk's own source)
+        unsigned long long base = 0;
+        for (unsigned long long c0 = 0; c0 < len; c0 += CMP_CAP) {
+            const unsigned cl = unsigned(min((unsigned long long)CMP_CAP, len - c0));
+            for (unsigned e = tid; e < cl; e += CMP_THREADS) {
+                s_c[e] = col[S + c0 + e];
+                s_v[e] = val[S + c0 + e];
+            }
+            __syncthreads();
+            for (unsigned cc = 0; cc < cl; cc += CMP_THREADS) {
+                const unsigned e = cc + tid;
+                const bool keep = e < cl && s_v[e] != 0.0;
+                const unsigned rank = block_exclusive_scan<CMP_THREADS>(keep ? 1u : 0u, s_warp, &s_total);
+                if (keep) {
+                    col[D + base + rank] = s_c[e];
+                    val[D + base + rank] = s_v[e];
+                }
+                base += s_total;
+                __syncthreads();
+            }
+        }
+        if (tid == 0) {
+            __threadfence();
+            atomicExch(&read_done[b], 1u);
+        }
+    }
+    __syncthreads();
+    }
+}
+
 
 // Optional CUDA events recorded around the row kernel (bench.py's per-kernel roofline).
 static thread_local cudaEvent_t g_timer_begin = nullptr, g_timer_end = nullptr;
@@ -926,8 +1145,12 @@ struct fa_plan {
     unsigned* sn1;
     unsigned* sn2;
     unsigned* ivptr;          // nv + 1
-    uint64_t* status;         // look-back tile status (nb)
-    unsigned long long* ticket;
+    uint64_t* status;         // look-back tile status (nb), then tickets and the compaction flag
+    unsigned long long* bsym; // nb: symbolic CSR segment start per bucket
+    unsigned* blen;           // nb
+    unsigned* bdrop;          // nb: exact-zero sums per bucket
+    unsigned long long* bshift;  // nb
+    unsigned* read_done;      // nb (k_compact)
     int64_t ninc;             // -1 until read back
     bool built;
 };
@@ -936,7 +1159,9 @@ using namespace fa;
 
 static void plan_free(fa_plan* p) {
     cudaFree(p->part_off); cudaFree(p->part_fill); cudaFree(p->M); cudaFree(p->rec); cudaFree(p->skey); cudaFree(p->sn1);
-    cudaFree(p->sn2); cudaFree(p->ivptr); cudaFree(p->status); cudaFree(p->ticket);
+    cudaFree(p->sn2); cudaFree(p->ivptr); cudaFree(p->status);
+    cudaFree(p->bsym); cudaFree(p->blen); cudaFree(p->bdrop); cudaFree(p->bshift); cudaFree(p->read_done);
+
 }
 
 static size_t place_smem_bytes(int nparts) {
@@ -984,8 +1209,15 @@ extern "C" int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t ro
     if (e == cudaSuccess) e = cudaMalloc(&p->sn1, sizeof(unsigned) * ninc_max);
     if (e == cudaSuccess) e = cudaMalloc(&p->sn2, sizeof(unsigned) * ninc_max);
     if (e == cudaSuccess) e = cudaMalloc(&p->ivptr, sizeof(unsigned) * (nv + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&p->status, sizeof(uint64_t) * (p->nb > 0 ? p->nb : 1));
-    if (e == cudaSuccess) e = cudaMalloc(&p->ticket, sizeof(unsigned long long));
+    // look-back status (nb) + the row-kernel ticket, the compaction ticket and scan flag
+    if (e == cudaSuccess) e = cudaMalloc(&p->status, sizeof(uint64_t) * ((p->nb > 0 ? p->nb : 1) + 4));
+    const size_t nbk = size_t(p->nb > 0 ? p->nb : 1);
+    if (e == cudaSuccess) e = cudaMalloc(&p->bsym, sizeof(unsigned long long) * nbk);
+    if (e == cudaSuccess) e = cudaMalloc(&p->blen, sizeof(unsigned) * nbk);
+    if (e == cudaSuccess) e = cudaMalloc(&p->bdrop, sizeof(unsigned) * nbk);
+    if (e == cudaSuccess) e = cudaMalloc(&p->bshift, sizeof(unsigned long long) * nbk);
+    if (e == cudaSuccess) e = cudaMalloc(&p->read_done, sizeof(unsigned) * nbk);
+
     if (e != cudaSuccess) {
         plan_free(p);
         delete p;
@@ -1007,14 +1239,17 @@ extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, 
     cudaStream_t st = as_stream(stream);
     p->ninc = -1;
     p->built = true;
-    k_reset_result<<<1, 32, 0, st>>>(d_res);
-    if (p->nb == 0) return FA_OK;
+    if (p->nb == 0) {
+        k_reset_result<<<1, 32, 0, st>>>(d_res);
+        return FA_OK;
+    }
+    k_reset<<<4, 256, 0, st>>>(d_res, p->part_off, p->nparts + 1, nullptr, 0);  // result + part counts
+    FA_LAUNCH_CHECK("k_reset");
     PlanArgs P;
     P.me = d_me; P.nme = p->nme; P.nq = p->nq; P.v0 = p->v0; P.v1 = p->v1;
     P.plog = p->plog; P.nparts = p->nparts; P.chunk = p->chunk_place;
     P.part_off = p->part_off; P.part_fill = p->part_fill; P.M = p->M; P.rec = p->rec;
     P.skey = p->skey; P.sn1 = p->sn1; P.sn2 = p->sn2; P.ivptr = p->ivptr; P.res = d_res;
-    FA_CUDA(cudaMemsetAsync(p->part_off, 0, sizeof(unsigned) * (p->nparts + 1), st));
     const size_t hist_smem = sizeof(unsigned) * p->nparts;
     FA_CUDA(cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_smem)));
     k_part_hist<<<p->nblk_place, PLAN_THREADS, hist_smem, st>>>(P);
@@ -1081,20 +1316,25 @@ extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double
     if (kind == FA_KIND_MASSW && !d_w) { set_error("WEIGHTED_MASS requires a WeightField"); return FA_ERR_ARGUMENT; }
     cudaStream_t st = as_stream(stream);
     const int64_t nrows = fa_plan_rows(p, kind);
-    k_reset_result<<<1, 32, 0, st>>>(d_res);
     if (nrows == 0 || p->nb == 0) {
+        k_reset_result<<<1, 32, 0, st>>>(d_res);
         FA_CUDA(cudaMemsetAsync(d_rowptr, 0, sizeof(int64_t), st));
         return FA_OK;
     }
-    FA_CUDA(cudaMemsetAsync(p->status, 0, sizeof(uint64_t) * p->nb, st));
-    FA_CUDA(cudaMemsetAsync(p->ticket, 0, sizeof(unsigned long long), st));
+    // result block, look-back status (nb), the row-kernel and compaction tickets and the
+    // compaction's scan flag (p->status has nb + 4 words)
+    k_reset<<<unsigned((p->nb + 4 + 255) / 256 < 64 ? (p->nb + 4 + 255) / 256 : 64), 256, 0, st>>>(
+        d_res, nullptr, 0, p->status, p->nb + 4);
+    FA_LAUNCH_CHECK("k_reset");
     RowsArgs A;
     A.skey = p->skey; A.sn1 = p->sn1; A.sn2 = p->sn2; A.ivptr = p->ivptr;
     A.q = reinterpret_cast<const double2*>(d_q); A.w = d_w; A.areas = d_areas;
     A.lam = lam; A.mu = mu;
     A.v0 = p->v0; A.v1 = p->v1; A.nrows = nrows;
     A.rowptr = d_rowptr; A.col = d_col; A.val = d_val; A.capacity = capacity;
-    A.status = p->status; A.ticket = p->ticket; A.res = d_res;
+    A.status = p->status; A.ticket = reinterpret_cast<unsigned long long*>(p->status + p->nb); A.res = d_res;
+    A.read_done = p->read_done;
+    A.bsym = p->bsym; A.blen = p->blen; A.bdrop = p->bdrop;
     int rc;
     switch (kind) {
         case FA_KIND_MASS: rc = launch_rows<FA_KIND_MASS>(A, p->nb, st); break;
@@ -1102,5 +1342,16 @@ extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double
         case FA_KIND_STIFF: rc = launch_rows<FA_KIND_STIFF>(A, p->nb, st); break;
         default: rc = launch_rows<FA_KIND_ELASTIC>(A, p->nb, st); break;
     }
-    return rc;
+    if (rc != FA_OK) return rc;
+    // exact-zero sums (if any) removed in place; exits at once when there are none
+    const int64_t rpb = int64_t(BV) * (kind == FA_KIND_ELASTIC ? 2 : 1);
+    const size_t cmp_smem = size_t(CMP_CAP) * (sizeof(double) + sizeof(int32_t));
+    FA_CUDA(cudaFuncSetAttribute(k_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cmp_smem)));
+    const unsigned cgrid = unsigned(p->nb < 2 * NUM_SMS_B200 ? p->nb : 2 * NUM_SMS_B200);
+    k_compact<<<cgrid, CMP_THREADS, cmp_smem, st>>>(p->bsym, p->blen, p->bdrop, p->bshift, p->read_done,
+                                                     reinterpret_cast<unsigned long long*>(p->status + p->nb + 1), p->nb,
+                                                     rpb, nrows, d_rowptr, d_col, d_val, d_res,
+                                                     reinterpret_cast<unsigned*>(p->status + p->nb + 2));
+    FA_LAUNCH_CHECK("k_compact");
+    return FA_OK;
 }

@@ -154,21 +154,23 @@ __device__ __forceinline__ T block_exclusive_scan(T v, T* warp_tot, T* total) {
 constexpr uint64_t LB_VALUE_MASK = (uint64_t(1) << 62) - 1;
 __device__ __forceinline__ uint64_t lb_pack(uint64_t flag, uint64_t v) { return (flag << 62) | v; }
 
-// Called by all threads of the block after the block aggregate is known.  Returns the
-// exclusive prefix of tile `tile` (sum of the aggregates of all earlier tiles).  Tiles must
-// be numbered in launch order via a ticket (fa::next_tile) so every predecessor is resident
-// or finished, which guarantees forward progress.
-__device__ __forceinline__ uint64_t lookback_prefix(uint64_t* status, int64_t tile, uint64_t aggregate,
-                                                     uint64_t* s_prefix) {
+// Publishes the aggregate of tile `tile` (thread 0); tile 0 publishes its inclusive prefix.
+__device__ __forceinline__ void lookback_publish(uint64_t* status, int64_t tile, uint64_t aggregate) {
+    if (threadIdx.x == 0) st_volatile_u64(&status[tile], lb_pack(tile == 0 ? 2 : 1, aggregate));
+}
+
+// Warp 0 only, after lookback_publish: writes the exclusive prefix of tile `tile` (sum of the
+// aggregates of all earlier tiles) to *s_prefix and publishes the inclusive prefix.  No block
+// barrier: the other warps continue; *s_prefix is valid after the caller's next
+// __syncthreads().  Tiles must be numbered in launch order via a ticket (fa::next_tile) so every
+// predecessor is resident or finished, which guarantees forward progress.
+__device__ __forceinline__ void lookback_resolve(uint64_t* status, int64_t tile, uint64_t aggregate,
+                                                 uint64_t* s_prefix) {
     if (threadIdx.x < 32) {
         const int lane = threadIdx.x;
         if (tile == 0) {
-            if (lane == 0) {
-                st_volatile_u64(&status[0], lb_pack(2, aggregate));
-                *s_prefix = 0;
-            }
+            if (lane == 0) *s_prefix = 0;
         } else {
-            if (lane == 0) st_volatile_u64(&status[tile], lb_pack(1, aggregate));
             uint64_t excl = 0;
             int64_t pred = tile - 1;
             unsigned backoff = 32;  // ns; doubles while predecessors are still empty (frees issue slots)
@@ -194,8 +196,19 @@ __device__ __forceinline__ uint64_t lookback_prefix(uint64_t* status, int64_t ti
             }
         }
     }
+}
+
+__device__ __forceinline__ uint64_t lookback_wait(uint64_t* status, int64_t tile, uint64_t aggregate,
+                                                  uint64_t* s_prefix) {
+    lookback_resolve(status, tile, aggregate, s_prefix);
     __syncthreads();
     return *s_prefix;
+}
+
+__device__ __forceinline__ uint64_t lookback_prefix(uint64_t* status, int64_t tile, uint64_t aggregate,
+                                                     uint64_t* s_prefix) {
+    lookback_publish(status, tile, aggregate);
+    return lookback_wait(status, tile, aggregate, s_prefix);
 }
 
 __device__ __forceinline__ int64_t next_tile(unsigned long long* ticket, int64_t* s_tile) {

@@ -178,3 +178,41 @@ def test_connectivity_out_of_range_is_reported():
     plan.build(torch.from_numpy(C).cuda())
     with pytest.raises(ValueError, match="out of range"):
         plan.check_build()
+
+
+def _structured_square(n):
+    """Unjittered, unpermuted right-triangle grid: stiffness off-diagonals across the
+    hypotenuse sum to exactly zero (Matlab drops them)."""
+    n1 = n + 1
+    x, y = np.meshgrid(np.linspace(0.0, 1.0, n1), np.linspace(0.0, 1.0, n1))
+    V = np.stack([x.ravel(), y.ravel()], axis=1)
+    cells = np.arange(n * n)
+    iy, ix = np.divmod(cells, n)
+    v00 = iy * n1 + ix
+    C = np.concatenate([np.stack([v00, v00 + 1, v00 + n1 + 1], 1), np.stack([v00, v00 + n1 + 1, v00 + n1], 1)])
+    return V, C
+
+
+@pytest.mark.parametrize("n", (8, 96, 400))
+def test_exact_zero_sums_are_compacted(n):
+    """Zero sums stay in the row kernel's symbolic layout and are removed by k_compact; the
+    result must equal the reference's dropped pattern (sparse.py:177-179) bit for bit, across
+    many buckets (n=400: 161k vertices, 1255 buckets)."""
+    V, C = _structured_square(n)
+    areas = fo.triangle_areas(V, C)
+    ref = c_oracle.assemble("stiff", V, C, areas, None, 1.0, 1.0)
+    got, r = plan_assemble("stiff", V, C, areas)
+    assert r.dropped > 0
+    assert_same_csc(got, ref, f"structured n={n}")
+
+
+def test_weighted_mass_zero_weights_are_compacted():
+    sm = seeded_square_mesh(200, 3)
+    areas = fo.triangle_areas(sm.vertices, sm.connectivity)
+    w = sm.weights.copy()
+    w[::3] = 0.0  # every third vertex weightless: entries among weightless vertices vanish
+    w[1::7] = -w[1::7]
+    ref = c_oracle.assemble("massw", sm.vertices, sm.connectivity, areas, w, 1.0, 1.0)
+    got, r = plan_assemble("massw", sm.vertices, sm.connectivity, areas, w)
+    assert r.dropped > 0
+    assert_same_csc(got, ref, "massw with zero weights")

@@ -8,6 +8,7 @@ from paper_1305_3122_b200 import _lib
 from paper_1305_3122_b200.device import ResultBlock
 from paper_1305_3122_b200.meshgen import seeded_square_mesh, BASELINE_CONFIGS
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
+NAMES = (sys.argv[2].split(",") if len(sys.argv) > 2 else ["p1", "p2", "p3", "p4", "p5"])
 kind, n, lam, mu = BASELINE_CONFIGS[cfg]
 sm = seeded_square_mesh(n, 0)
 dev = torch.device("cuda")
@@ -31,10 +32,9 @@ lib.fa_debug_timeline(buf.ctypes.data, buf.size)
 t = buf[: nb * 6].reshape(nb, 6).astype(np.int64)
 t0 = t[:, 0].min()
 t = t - t0
-t[:, 4] = t[:, 3]
 d = np.diff(t, axis=1)
 print("kernel span us", (t[:, 5].max()) / 1e3)
-for i, name in enumerate(["a (records)", "c (accumulate)", "zero-scan+cols", "-", "copy"]):
+for i, name in enumerate(NAMES):
     print(f"{name:16s} mean {d[:, i].mean()/1e3:7.2f} us  p50 {np.median(d[:, i])/1e3:7.2f}  p90 {np.percentile(d[:, i], 90)/1e3:7.2f}")
 print("block duration mean", (t[:, 5] - t[:, 0]).mean() / 1e3, "us; start spread", t[:, 0].max() / 1e3)
 conc = np.zeros(200)
