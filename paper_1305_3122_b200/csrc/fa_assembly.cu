@@ -440,18 +440,24 @@ struct Gathered {
 };
 
 template <int KIND>
-__device__ __forceinline__ Gathered gather_incidence(const RowsArgs& A, unsigned k, unsigned n1, unsigned n2) {
+__device__ __forceinline__ Gathered gather_incidence(const RowsArgs& A, unsigned k, unsigned n1, unsigned n2,
+                                                     uint64_t pol) {
     Gathered g;
+#ifdef FA_EXP_NOGATHER
+    g.p1 = make_double2(double(n1), 1.0); g.p2 = make_double2(double(n2), 2.0);
+    g.w1 = double(n1 + 1); g.w2 = double(n2 + 1); g.ar = double(k + 1) * 1e-6;
+    return g;
+#endif
     g.p1 = g.p2 = make_double2(0.0, 0.0);
     g.w1 = g.w2 = 0.0;
-    g.ar = A.areas ? A.areas[k] : 0.0;
+    g.ar = A.areas ? ld_keep_f64(A.areas + k, pol) : 0.0;
     if (KIND == FA_KIND_STIFF || KIND == FA_KIND_ELASTIC || !A.areas) {
-        g.p1 = A.q[n1];
-        g.p2 = A.q[n2];
+        g.p1 = ld_keep_f64x2(A.q + n1, pol);
+        g.p2 = ld_keep_f64x2(A.q + n2, pol);
     }
     if (KIND == FA_KIND_MASSW) {
-        g.w1 = A.w[n1];
-        g.w2 = A.w[n2];
+        g.w1 = ld_keep_f64(A.w + n1, pol);
+        g.w2 = ld_keep_f64(A.w + n2, pol);
     }
     return g;
 }
@@ -597,7 +603,7 @@ __device__ __noinline__ RowCount general_row(const RowsArgs& A, BucketRecs R, bo
         n1 = int(A.sn1[gfirst + i]);
         n2 = int(A.sn2[gfirst + i]);
         if (need_vals) {
-            const Gathered g = gather_incidence<KIND>(A, ka >> 2, unsigned(n1), unsigned(n2));
+            const Gathered g = gather_incidence<KIND>(A, ka >> 2, unsigned(n1), unsigned(n2), l2_evict_last_policy());
             incidence_values<KIND>(A, ka >> 2, a, g, own_p, own_w, rv);
         }
     };
@@ -693,6 +699,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
 
     const int tid = threadIdx.x;
     const uint64_t pol_first = l2_evict_first_policy();
+    const uint64_t pol_last = l2_evict_last_policy();
     const int64_t b = next_tile(A.ticket, &s_tile);  // bucket, in launch order
     TL(b, 0);
     const int64_t nvl = A.v1 - A.v0;
@@ -712,10 +719,27 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     for (int vl = tid; vl < nvb && !overflow; vl += NT)
         for (int j = s_vst[vl]; j < s_vst[vl + 1]; ++j) s_own[j] = (unsigned char)vl;
     // ---- s) the bucket's plan entries -> shared memory (coalesced)
-    for (int i = tid; i < n; i += NT) {
-        R.ka[i] = ld_stream_u32(A.skey + gbase + i, pol_first);
-        R.n1[i] = int(ld_stream_u32(A.sn1 + gbase + i, pol_first));
-        R.n2[i] = int(ld_stream_u32(A.sn2 + gbase + i, pol_first));
+    {  // all loads of a thread issued before the first store (one DRAM round trip)
+        constexpr int PER = CAPB / NT;
+        unsigned lk[PER], l1[PER], l2[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int i = tid + u * NT;
+            if (i < n) {
+                lk[u] = ld_stream_u32(A.skey + gbase + i, pol_first);
+                l1[u] = ld_stream_u32(A.sn1 + gbase + i, pol_first);
+                l2[u] = ld_stream_u32(A.sn2 + gbase + i, pol_first);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int i = tid + u * NT;
+            if (i < n) {
+                R.ka[i] = lk[u];
+                R.n1[i] = int(l1[u]);
+                R.n2[i] = int(l2[u]);
+            }
+        }
     }
     __syncthreads();
 
@@ -771,7 +795,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
             for (int u = 0; u < AU; ++u) {
                 const int i = i0 + u * NT;
                 ka[u] = i < n ? R.ka[i] : 0u;
-                if (i < n) g[u] = gather_incidence<KIND>(A, ka[u] >> 2, unsigned(R.n1[i]), unsigned(R.n2[i]));
+                if (i < n) g[u] = gather_incidence<KIND>(A, ka[u] >> 2, unsigned(R.n1[i]), unsigned(R.n2[i]), pol_last);
             }
 #pragma unroll
             for (int u = 0; u < AU; ++u) {
