@@ -57,6 +57,8 @@ constexpr int PLOG0 = 10;          // log2 of the minimum part size (vertices)
 constexpr int MAX_PARTS = 8192;
 constexpr int PLAN_THREADS = 1024;
 constexpr int SORT_THREADS = 512;   // k_part_sort (2 blocks / SM, 64 registers)
+constexpr int PLACE_THREADS = 1024;  // k_part_hist / k_part_place block size
+constexpr int PLACE_BLOCKS_PER_SM = 1;
 constexpr int PLACE_TRI = 2048;    // triangles per placement round
 constexpr int SORT_CAP = 7680;     // part incidences sorted in shared memory (2 blocks / SM)
 
@@ -119,27 +121,37 @@ struct PlanArgs {
 
 // K1: owned incidences per (block, part) and per part; index validation (sparse.py:131-137 semantics: first bad
 // position in the flattened connectivity).
-__global__ void __launch_bounds__(PLAN_THREADS) k_part_hist(const __grid_constant__ PlanArgs P) {
+__global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_constant__ PlanArgs P) {
     extern __shared__ unsigned s_cnt[];
-    for (int i = threadIdx.x; i < P.nparts; i += PLAN_THREADS) s_cnt[i] = 0;
+    for (int i = threadIdx.x; i < P.nparts; i += PLACE_THREADS) s_cnt[i] = 0;
     __syncthreads();
     const int64_t k0 = int64_t(blockIdx.x) * P.chunk, k1 = min(P.nme, k0 + P.chunk);
-    for (int64_t k = k0 + threadIdx.x; k < k1; k += PLAN_THREADS) {
-        int c[3];
-        load_tri_ids(P.me, k, c[0], c[1], c[2]);
+    constexpr int U = 4;  // triangles in flight per thread
+    for (int64_t k0u = k0 + threadIdx.x; k0u < k1; k0u += U * PLACE_THREADS) {
+        int c[U][3];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-            const int64_t v = c[a];
-            if (v < 0 || v >= P.nq) {
-                atomic_min_i64(&P.res->index_error_pos, 3 * k + a);
-                continue;
+        for (int u = 0; u < U; ++u) {
+            const int64_t k = k0u + u * PLACE_THREADS;
+            if (k < k1) load_tri_ids(P.me, k, c[u][0], c[u][1], c[u][2]);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t k = k0u + u * PLACE_THREADS;
+            if (k >= k1) break;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                const int64_t v = c[u][a];
+                if (v < 0 || v >= P.nq) {
+                    atomic_min_i64(&P.res->index_error_pos, 3 * k + a);
+                    continue;
+                }
+                if (v >= P.v0 && v < P.v1) atomicAdd(&s_cnt[(v - P.v0) >> P.plog], 1u);
             }
-            if (v >= P.v0 && v < P.v1) atomicAdd(&s_cnt[(v - P.v0) >> P.plog], 1u);
         }
     }
     __syncthreads();
     unsigned* row = P.M + int64_t(blockIdx.x) * P.nparts;
-    for (int i = threadIdx.x; i < P.nparts; i += PLAN_THREADS) {
+    for (int i = threadIdx.x; i < P.nparts; i += PLACE_THREADS) {
         row[i] = s_cnt[i];
         if (s_cnt[i]) atomicAdd(&P.part_off[i], s_cnt[i]);
     }
@@ -174,35 +186,35 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_part_scan(const __grid_constan
 // (count matrix row of K1, one atomic per part); per round of PLACE_TRI triangles the records
 // are ranked by part in shared memory, staged in part order and written as coalesced runs.
 // Order inside a part is arbitrary (K4 sorts).
-__global__ void __launch_bounds__(PLAN_THREADS, 1) k_part_place(const __grid_constant__ PlanArgs P) {
+__global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_place(const __grid_constant__ PlanArgs P) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int RI = 3 * PLACE_TRI;                  // incidences per round
-    constexpr int TPT = PLACE_TRI / PLAN_THREADS;      // triangles per thread per round
+    constexpr int TPT = PLACE_TRI / PLACE_THREADS;      // triangles per thread per round
     uint4* s_stage = reinterpret_cast<uint4*>(smem_raw);                    // [RI]
     unsigned* s_cnt = reinterpret_cast<unsigned*>(s_stage + RI);            // [nparts] round counts
     unsigned* s_lst = s_cnt + P.nparts;                                     // [nparts] round local starts
     unsigned* s_gb = s_lst + P.nparts;                                      // [nparts] global cursor
     unsigned short* s_part = reinterpret_cast<unsigned short*>(s_gb + P.nparts);  // [RI]
-    __shared__ unsigned s_warp[PLAN_THREADS / 32];
+    __shared__ unsigned s_warp[PLACE_THREADS / 32];
     __shared__ unsigned s_total;
     const int tid = threadIdx.x;
     const int64_t kb0 = int64_t(blockIdx.x) * P.chunk, kb1 = min(P.nme, kb0 + P.chunk);
     const int pmask = (1 << P.plog) - 1;
     {
         const unsigned* row = P.M + int64_t(blockIdx.x) * P.nparts;
-        for (int i = tid; i < P.nparts; i += PLAN_THREADS) {
+        for (int i = tid; i < P.nparts; i += PLACE_THREADS) {
             const unsigned c = row[i];
             s_gb[i] = c ? atomicAdd(&P.part_fill[i], c) : 0u;
         }
     }
     for (int64_t r0 = kb0; r0 < kb1; r0 += PLACE_TRI) {
-        for (int i = tid; i < P.nparts; i += PLAN_THREADS) s_cnt[i] = 0;
+        for (int i = tid; i < P.nparts; i += PLACE_THREADS) s_cnt[i] = 0;
         __syncthreads();
         uint4 rec[3 * TPT];
         unsigned part[3 * TPT], rank[3 * TPT];
 #pragma unroll
         for (int t = 0; t < TPT; ++t) {
-            const int64_t k = r0 + t * PLAN_THREADS + tid;
+            const int64_t k = r0 + t * PLACE_THREADS + tid;
             int c[3] = {-1, -1, -1};
             if (k < kb1) load_tri_ids(P.me, k, c[0], c[1], c[2]);
 #pragma unroll
@@ -221,20 +233,19 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) k_part_place(const __grid_con
         }
         __syncthreads();
         // local starts: exclusive scan of the round counts over parts
-        constexpr int PER = MAX_PARTS / PLAN_THREADS;
-        unsigned cl[PER], run = 0;
-#pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            const int i = tid * PER + j;
-            cl[j] = i < P.nparts ? s_cnt[i] : 0u;
-            run += cl[j];
+        const int per = (P.nparts + PLACE_THREADS - 1) / PLACE_THREADS;
+        unsigned run = 0;
+        for (int j = 0; j < per; ++j) {
+            const int i = tid * per + j;
+            run += i < P.nparts ? s_cnt[i] : 0u;
         }
-        unsigned ex = block_exclusive_scan<PLAN_THREADS>(run, s_warp, &s_total);
-#pragma unroll
-        for (int j = 0; j < PER; ++j) {
-            const int i = tid * PER + j;
-            if (i < P.nparts) s_lst[i] = ex;
-            ex += cl[j];
+        unsigned ex = block_exclusive_scan<PLACE_THREADS>(run, s_warp, &s_total);
+        for (int j = 0; j < per; ++j) {
+            const int i = tid * per + j;
+            if (i < P.nparts) {
+                s_lst[i] = ex;
+                ex += s_cnt[i];
+            }
         }
         __syncthreads();
 #pragma unroll
@@ -247,7 +258,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) k_part_place(const __grid_con
         }
         __syncthreads();
         const int total = int(s_total);
-        for (int i = tid; i < total; i += PLAN_THREADS) {
+        for (int i = tid; i < total; i += PLACE_THREADS) {
             const unsigned p = s_part[i];
             const unsigned g = s_gb[p] + (unsigned(i) - s_lst[p]);
             const uint4 r = s_stage[i];
@@ -256,7 +267,7 @@ __global__ void __launch_bounds__(PLAN_THREADS, 1) k_part_place(const __grid_con
                          : "memory");
         }
         __syncthreads();
-        for (int i = tid; i < P.nparts; i += PLAN_THREADS) s_gb[i] += s_cnt[i];
+        for (int i = tid; i < P.nparts; i += PLACE_THREADS) s_gb[i] += s_cnt[i];
     }
 }
 
@@ -1220,7 +1231,7 @@ extern "C" int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t ro
     while (((nv + (int64_t(1) << p->plog) - 1) >> p->plog) > MAX_PARTS) ++p->plog;
     p->nparts = int((nv + (int64_t(1) << p->plog) - 1) >> p->plog);
     if (p->nparts < 1) p->nparts = 1;
-    p->chunk_place = (nme + NUM_SMS_B200 - 1) / NUM_SMS_B200;
+    p->chunk_place = (nme + PLACE_BLOCKS_PER_SM * NUM_SMS_B200 - 1) / (PLACE_BLOCKS_PER_SM * NUM_SMS_B200);
     p->nblk_place = int((nme + p->chunk_place - 1) / p->chunk_place);
     p->ninc = -1;
     const size_t ninc_max = size_t(3) * size_t(nme);
@@ -1276,13 +1287,13 @@ extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, 
     P.skey = p->skey; P.sn1 = p->sn1; P.sn2 = p->sn2; P.ivptr = p->ivptr; P.res = d_res;
     const size_t hist_smem = sizeof(unsigned) * p->nparts;
     FA_CUDA(cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_smem)));
-    k_part_hist<<<p->nblk_place, PLAN_THREADS, hist_smem, st>>>(P);
+    k_part_hist<<<p->nblk_place, PLACE_THREADS, hist_smem, st>>>(P);
     FA_LAUNCH_CHECK("k_part_hist");
     k_part_scan<<<1, PLAN_THREADS, 0, st>>>(P);
     FA_LAUNCH_CHECK("k_part_scan");
     const size_t place_smem = place_smem_bytes(p->nparts);
     FA_CUDA(cudaFuncSetAttribute(k_part_place, cudaFuncAttributeMaxDynamicSharedMemorySize, int(place_smem)));
-    k_part_place<<<p->nblk_place, PLAN_THREADS, place_smem, st>>>(P);
+    k_part_place<<<p->nblk_place, PLACE_THREADS, place_smem, st>>>(P);
     FA_LAUNCH_CHECK("k_part_place");
     const size_t sort_smem = sort_smem_bytes(p->plog);
     FA_CUDA(cudaFuncSetAttribute(k_part_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sort_smem)));

@@ -42,6 +42,17 @@ for i in range(n):
     key = (seq[i] or "?").split("[")[-1].split(":")[0]
     aggf[key] += e; stlf[key] += s
 te, ts = sum(agg.values()), sum(stl.values())
+if os.environ.get("PHASES"):  # "name:lo-hi,name:lo-hi" line ranges of the kernel file (outer line)
+    ph = [(nm, int(r.split("-")[0]), int(r.split("-")[1])) for nm, r in (x.split(":") for x in os.environ["PHASES"].split(","))]
+    pe, ps = collections.Counter(), collections.Counter()
+    for k in agg:
+        try:
+            ln = int(k.split(" ")[0].split(":")[1])
+        except (IndexError, ValueError):
+            ln = -1
+        nm = next((n for n, lo, hi in ph if lo <= ln <= hi), "other")
+        pe[nm] += agg[k]; ps[nm] += stl[k]
+    print("by phase:", {k: f"{v/te*100:.1f}% inst / {ps[k]/ts*100:.1f}% stall" for k, v in pe.most_common()})
 print("by file:", {k: f"{v/te*100:.1f}%/{stlf[k]/ts*100:.1f}%" for k, v in aggf.most_common()})
 for k, v in agg.most_common(int(os.environ.get("TOP", 40))):
     print(f"{v/te*100:5.1f}% inst {stl[k]/ts*100:5.1f}% stall  {k}")
