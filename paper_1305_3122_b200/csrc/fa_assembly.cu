@@ -51,7 +51,10 @@
 namespace fa {
 
 constexpr int BV = 128;            // vertices per row bucket
-constexpr int CAPB = 8 * BV;       // incidences per bucket held in shared memory
+#ifndef FA_CAPB
+#define FA_CAPB (8 * BV)
+#endif
+constexpr int CAPB = FA_CAPB;      // incidences per bucket held in shared memory
 constexpr int MAXD = 8;            // incidences per row on the register fast path
 constexpr int PLOG0 = 10;          // log2 of the minimum part size (vertices)
 constexpr int MAX_PARTS = 8192;
@@ -731,7 +734,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         for (int j = s_vst[vl]; j < s_vst[vl + 1]; ++j) s_own[j] = (unsigned char)vl;
     // ---- s) the bucket's plan entries -> shared memory (coalesced)
     {  // all loads of a thread issued before the first store (one DRAM round trip)
-        constexpr int PER = CAPB / NT;
+        constexpr int PER = (CAPB + NT - 1) / NT;
         unsigned lk[PER], l1[PER], l2[PER];
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
