@@ -152,6 +152,12 @@ int fa_triplets_to_csc(const int64_t* d_rows, const int64_t* d_cols, const doubl
                        int64_t* d_rowidx, double* d_vals_out, void* d_workspace,
                        size_t workspace_bytes, fa_result* d_result, void* stream);
 
+/* CSC (col_ptr, row_idx int64; values f64; host arrays) -> coordinate MatrixMarket file, byte
+ * identical to femasm's write_matrix_market (pkg/src/femasm/sparse.py:332-339): 1-based "i j v"
+ * lines in CSC order, values "%.17g".  threads <= 0: all hardware threads.  Host only. */
+int fa_write_matrix_market(const char* path, int64_t n_rows, int64_t n_cols, const int64_t* col_ptr,
+                           const int64_t* row_idx, const double* values, int threads);
+
 /* ------------------------------------------------------------------------------------
  * Diagnostics.  fa_selftest_division compares the library's call-free correctly rounded
  * fp64 division (used by every element value) bitwise with CUDA's __ddiv_rn on n generated

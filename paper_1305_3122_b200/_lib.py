@@ -47,6 +47,7 @@ EXPORTED_SYMBOLS = (
     "fa_triplets_to_csc",
     "fa_selftest_division",
     "fa_set_kernel_timer",
+    "fa_write_matrix_market",
 )
 
 
@@ -89,6 +90,7 @@ _SIGNATURES = {
     "fa_triplets_to_csc": (_I, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, ctypes.c_size_t, _P, _P]),
     "fa_selftest_division": (_I, [_I64, ctypes.c_uint64, _P, _P, _P]),
     "fa_set_kernel_timer": (_I, [_P, _P]),
+    "fa_write_matrix_market": (_I, [ctypes.c_char_p, _I64, _I64, _P, _P, _P, _I]),
 }
 
 _lib = None

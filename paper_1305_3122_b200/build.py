@@ -16,7 +16,7 @@ from pathlib import Path
 PKG_DIR = Path(__file__).resolve().parent
 CSRC = PKG_DIR / "csrc"
 OUT = PKG_DIR / "libfemasm_b200.so"
-SOURCES = ["fa_capi.cu", "fa_assembly.cu", "fa_batch.cu", "fa_triplets.cu", "fa_selftest.cu"]
+SOURCES = ["fa_capi.cu", "fa_assembly.cu", "fa_batch.cu", "fa_triplets.cu", "fa_selftest.cu", "fa_io.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -14,6 +14,8 @@ from __future__ import annotations
 
 from dataclasses import dataclass
 
+import os
+
 import numpy as np
 
 from . import _lib
@@ -334,13 +336,19 @@ class TripletBatch:
         return csc_from_triplets(i, j, k, n_rows, n_cols)
 
 
-def write_matrix_market(matrix: CscMatrix, path) -> None:
-    """Coordinate MatrixMarket, 1-based, values with 17 significant digits (sparse.py:332-339)."""
-    rows, cols, vals = matrix.triplets()
-    with open(path, "w", encoding="ascii") as f:
-        f.write("%%MatrixMarket matrix coordinate real general\n")
-        f.write(f"{matrix.n_rows} {matrix.n_cols} {matrix.nnz}\n")
-        if rows.size:
-            body = np.char.mod("%d", rows + 1).astype(object) + " " + np.char.mod("%d", cols + 1).astype(object) + " " + \
-                np.array(["%.17g" % v for v in vals], dtype=object)
-            f.write("\n".join(body.tolist()) + "\n")
+def write_matrix_market(matrix: CscMatrix, path, threads: int = 0) -> None:
+    """Coordinate MatrixMarket, 1-based, values "%.17g", entries in CSC order - the file of
+    femasm's write_matrix_market (sparse.py:332-339) byte for byte, written by the library's
+    multi-threaded host writer (fa_write_matrix_market; no GPU needed)."""
+    import ctypes
+
+    from . import _lib
+
+    cp = np.ascontiguousarray(matrix.col_ptr, dtype=np.int64)
+    ri = np.ascontiguousarray(matrix.row_idx, dtype=np.int64)
+    va = np.ascontiguousarray(matrix.values, dtype=np.float64)
+    rc = _lib.lib().fa_write_matrix_market(os.fsencode(os.fspath(path)), matrix.n_rows, matrix.n_cols,
+                                           cp.ctypes.data_as(ctypes.c_void_p), ri.ctypes.data_as(ctypes.c_void_p),
+                                           va.ctypes.data_as(ctypes.c_void_p), int(threads))
+    if rc != 0:
+        raise OSError(_lib.last_error())

@@ -82,6 +82,45 @@ def test_matrix_market_writer(tmp_path):
     assert np.array_equal(scipy.io.mmread(p).toarray(), a.to_dense())
 
 
+def _reference_mtx(matrix, path):
+    """femasm's writer, restated from sparse.py:332-339 (per-entry Python loop)."""
+    rows, cols, vals = matrix.triplets()
+    with open(path, "w", encoding="ascii") as f:
+        f.write("%%MatrixMarket matrix coordinate real general\n")
+        f.write(f"{matrix.n_rows} {matrix.n_cols} {matrix.nnz}\n")
+        for i, j, v in zip(rows, cols, vals):
+            f.write(f"{i + 1} {j + 1} {'%.17g' % v}\n")
+
+
+@pytest.mark.parametrize("threads", (1, 3, 0))
+def test_matrix_market_writer_is_byte_identical(tmp_path, threads):
+    rng = np.random.default_rng(7)
+    n_rows, n_cols = 500, 300
+    dense = np.zeros((n_rows, n_cols))
+    mask = rng.random((n_rows, n_cols)) < 0.05
+    vals = rng.standard_normal(mask.sum()) * 10.0 ** rng.integers(-320, 300, mask.sum())
+    special = np.array([1.0, -0.0, 0.1, 1e-5, 123456789.0, 2.0 ** -1074, 1.7976931348623157e308, -2.5])
+    vals[: special.size] = special
+    dense[mask] = vals
+    dense[:, 17] = 0.0  # empty columns inside and at the end
+    dense[:, -1] = 0.0
+    nz = dense != 0.0
+    nz[mask] = True
+    nz[:, 17] = False
+    nz[:, -1] = False
+    cols = np.nonzero(nz.T)
+    col_ptr = np.concatenate([[0], np.cumsum(nz.sum(axis=0))])
+    a = fa.CscMatrix(n_rows, n_cols, col_ptr, cols[1], dense.T[nz.T])
+    ours, ref = tmp_path / "ours.mtx", tmp_path / "ref.mtx"
+    fa.write_matrix_market(a, ours, threads=threads)
+    _reference_mtx(a, ref)
+    assert ours.read_bytes() == ref.read_bytes()
+    empty = fa.CscMatrix(4, 3, np.zeros(4, dtype=np.int64), [], [])
+    fa.write_matrix_market(empty, ours, threads=threads)
+    _reference_mtx(empty, ref)
+    assert ours.read_bytes() == ref.read_bytes()
+
+
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU behaviour")
 def test_no_cpu_fallback_without_gpu():
     with pytest.raises(RuntimeError, match="CUDA"):
