@@ -210,16 +210,33 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
             s_gb[i] = c ? atomicAdd(&P.part_fill[i], c) : 0u;
         }
     }
+    // triangle ids of the next round are loaded while the current one is placed
+    int nxt[TPT][3];
+#pragma unroll
+    for (int t = 0; t < TPT; ++t) {
+        const int64_t k = kb0 + t * PLACE_THREADS + tid;
+        nxt[t][0] = nxt[t][1] = nxt[t][2] = -1;
+        if (k < kb1) load_tri_ids(P.me, k, nxt[t][0], nxt[t][1], nxt[t][2]);
+    }
     for (int64_t r0 = kb0; r0 < kb1; r0 += PLACE_TRI) {
         for (int i = tid; i < P.nparts; i += PLACE_THREADS) s_cnt[i] = 0;
+        int cur[TPT][3];
+#pragma unroll
+        for (int t = 0; t < TPT; ++t) {
+            cur[t][0] = nxt[t][0];
+            cur[t][1] = nxt[t][1];
+            cur[t][2] = nxt[t][2];
+            const int64_t k = r0 + PLACE_TRI + t * PLACE_THREADS + tid;
+            nxt[t][0] = nxt[t][1] = nxt[t][2] = -1;
+            if (k < kb1) load_tri_ids(P.me, k, nxt[t][0], nxt[t][1], nxt[t][2]);
+        }
         __syncthreads();
         uint4 rec[3 * TPT];
         unsigned part[3 * TPT], rank[3 * TPT];
 #pragma unroll
         for (int t = 0; t < TPT; ++t) {
             const int64_t k = r0 + t * PLACE_THREADS + tid;
-            int c[3] = {-1, -1, -1};
-            if (k < kb1) load_tri_ids(P.me, k, c[0], c[1], c[2]);
+            const int c[3] = {cur[t][0], cur[t][1], cur[t][2]};
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 const int64_t v = c[a];
