@@ -350,7 +350,20 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_cons
     const uint64_t pol = l2_evict_first_policy();
     for (int i = tid; i < PV; i += SORT_THREADS) s_cur[i] = 0;
     __syncthreads();
-    for (unsigned i = tid; i < n; i += SORT_THREADS) atomicAdd(&s_cur[P.rec[off + i].y >> 2], 1u);
+    {  // vertex counts: eight records in flight per thread
+        const unsigned* ry = reinterpret_cast<const unsigned*>(P.rec + off) + 1;  // .y fields
+        for (unsigned i0 = tid; i0 < n; i0 += 8 * SORT_THREADS) {
+            unsigned y[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const unsigned i = i0 + u * SORT_THREADS;
+                y[u] = i < n ? ry[4 * size_t(i)] : 0xffffffffu;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (y[u] != 0xffffffffu) atomicAdd(&s_cur[y[u] >> 2], 1u);
+        }
+    }
     __syncthreads();
     // vertex starts: thread t scans PV / 1024 consecutive vertices
     const int per = PV / SORT_THREADS;
@@ -370,15 +383,25 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_cons
     unsigned* n1 = fast ? s_dyn + PV + SORT_CAP : P.sn1 + off;
     unsigned* n2 = fast ? s_dyn + PV + 2 * SORT_CAP : P.sn2 + off;
     unsigned short* s_src = reinterpret_cast<unsigned short*>(s_dyn + PV + 3 * SORT_CAP);  // fast: [SORT_CAP]
-    for (unsigned i = tid; i < n; i += SORT_THREADS) {
-        uint4 r;
-        asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
-                     : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                     : "l"(P.rec + off + i), "l"(pol));
-        const unsigned pos = atomicAdd(&s_cur[r.y >> 2], 1u);
-        key[pos] = (r.x << 2) | (r.y & 3u);
-        n1[pos] = r.z;
-        n2[pos] = r.w;
+    for (unsigned i0 = tid; i0 < n; i0 += 4 * SORT_THREADS) {  // four records in flight per thread
+        uint4 r[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const unsigned i = i0 + u * SORT_THREADS;
+            if (i < n)
+                asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                             : "=r"(r[u].x), "=r"(r[u].y), "=r"(r[u].z), "=r"(r[u].w)
+                             : "l"(P.rec + off + i), "l"(pol));
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            if (i0 + u * SORT_THREADS < n) {
+                const unsigned pos = atomicAdd(&s_cur[r[u].y >> 2], 1u);
+                key[pos] = (r[u].x << 2) | (r[u].y & 3u);
+                n1[pos] = r[u].z;
+                n2[pos] = r[u].w;
+            }
+        }
     }
     __syncthreads();
     if (fast) {
