@@ -662,6 +662,7 @@ __device__ __noinline__ RowCount general_row(const RowsArgs& A, BucketRecs R, bo
         }
     };
     int64_t last = -1, count = 0, zeros = 0;
+    if (deg == 0) return RowCount{0, 0};  // a vertex no triangle references has an empty row
     while (true) {
         int64_t c = INT64_MAX;  // next vertex column
         if (v > last) c = v;
@@ -826,7 +827,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
             if (c != 0xffffffffu && c != prev) ++distinct;
             prev = c;
         }
-        count = int64_t(NV) * (distinct + 1);
+        count = deg == 0 ? 0 : int64_t(NV) * (distinct + 1);  // no triplet, no entry (isolated vertex)
     }
     if (EARLY && slow)
         count = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc], s_ow[vloc], s, 0,
@@ -1272,6 +1273,12 @@ extern "C" int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t ro
     p->nb = (nv + BV - 1) / BV;
     p->plog = PLOG0;
     while (((nv + (int64_t(1) << p->plog) - 1) >> p->plog) > MAX_PARTS) ++p->plog;
+    // test hook: FEMASM_B200_PART_LOG2 forces larger parts, i.e. the plan's general (global
+    // memory) sort path that very large row blocks take
+    if (const char* env = getenv("FEMASM_B200_PART_LOG2")) {
+        const int forced = atoi(env);
+        if (forced > p->plog && forced <= 20) p->plog = forced;
+    }
     p->nparts = int((nv + (int64_t(1) << p->plog) - 1) >> p->plog);
     if (p->nparts < 1) p->nparts = 1;
     p->chunk_place = (nme + PLACE_BLOCKS_PER_SM * NUM_SMS_B200 - 1) / (PLACE_BLOCKS_PER_SM * NUM_SMS_B200);

@@ -216,3 +216,34 @@ def test_weighted_mass_zero_weights_are_compacted():
     got, r = plan_assemble("massw", sm.vertices, sm.connectivity, areas, w)
     assert r.dropped > 0
     assert_same_csc(got, ref, "massw with zero weights")
+
+
+@pytest.mark.parametrize("part_log2", (11, 13))
+@pytest.mark.parametrize("kind", KINDS)
+def test_large_part_general_sort_path(monkeypatch, kind, part_log2):
+    """Parts above 1024 vertices (row blocks above 8.4M vertices) are sorted in global memory;
+    forced here on a small mesh (with high-degree vertices mixed in) and checked bitwise."""
+    monkeypatch.setenv("FEMASM_B200_PART_LOG2", str(part_log2))
+    sm = seeded_square_mesh(48, 2)
+    V, C = sm.vertices, sm.connectivity
+    Vf, Cf = fan_mesh(40)
+    V = np.concatenate([V, Vf + 2.0])
+    C = np.concatenate([C, Cf + sm.nq])
+    areas = fo.triangle_areas(V, C)
+    w = 0.5 + np.arange(V.shape[0]) % 7 * 0.25
+    ref = c_oracle.assemble(kind, V, C, areas, w, 2.0, 0.7)
+    got, _ = plan_assemble(kind, V, C, areas, w, 2.0, 0.7)
+    assert_same_csc(got, ref, f"{kind} part_log2={part_log2}")
+
+
+def test_isolated_vertices_have_empty_rows():
+    """A vertex no triangle references has no triplet, hence an empty row (reference)."""
+    sm = seeded_square_mesh(8, 1)
+    V = np.concatenate([sm.vertices, [[5.0, 5.0], [6.0, 6.0]]])
+    C = np.asarray(sm.connectivity)
+    areas = fo.triangle_areas(V, C)
+    w = np.ones(V.shape[0])
+    for kind in KINDS:
+        ref = c_oracle.assemble(kind, V, C, areas, w, 1.0, 0.5)
+        got, _ = plan_assemble(kind, V, C, areas, w, 1.0, 0.5)
+        assert_same_csc(got, ref, kind)
