@@ -61,6 +61,7 @@ def parse_args():
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-baseline-runs", type=int, default=2, help="timed runs of the 1-core CPU baseline (0: skip)")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--graph", type=int, default=1, help="replay each step as a captured CUDA graph (N=1)")
     return ap.parse_args()
 
 
@@ -310,20 +311,45 @@ def run_ours(args):
 
     def step(cold=True):
         if cold:
-            plan.build(me_d, stream)
-        plan.assemble_into(kind, q_use, a_d, w_d, lam, mu, rowptr, col, val, res, stream)
+            plan.build(me_d)  # current stream (the capture stream inside a graph capture)
+        plan.assemble_into(kind, q_use, a_d, w_d, lam, mu, rowptr, col, val, res)
         if world > 1:
             dist.all_gather_into_tensor(nnz_t, rowptr[-1:])  # row-offset allgather (NCCL)
+
+    # one cold (or warm) step captured as a CUDA graph: the launches of the ~8 kernels of a
+    # step are replayed without host round trips (the kernel timer events are graph nodes)
+    graphs = {}
+
+    def graph_for(cold):
+        if cold not in graphs:
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                step(cold)  # warm the capture stream
+            torch.cuda.current_stream().wait_stream(side)
+            torch.cuda.synchronize()
+            lib.fa_set_kernel_timer(ctypes_ptr(ev_rows0), ctypes_ptr(ev_rows1))
+            with torch.cuda.graph(g):
+                step(cold)
+            lib.fa_set_kernel_timer(None, None)
+            torch.cuda.synchronize()
+            graphs[cold] = g
+        return graphs[cold]
 
     def timed_loop(steps, cold):
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         ends = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
         rows_ms = []
+        g = graph_for(cold) if use_graph else None
         for i in range(steps):
             flush.zero_()
             starts[i].record()
-            lib.fa_set_kernel_timer(ctypes_ptr(ev_rows0), ctypes_ptr(ev_rows1))
-            step(cold)
+            if g is not None:
+                g.replay()
+            else:
+                lib.fa_set_kernel_timer(ctypes_ptr(ev_rows0), ctypes_ptr(ev_rows1))
+                step(cold)
             ends[i].record()
             torch.cuda.synchronize()
             rows_ms.append(ev_rows0.elapsed_time(ev_rows1))
@@ -333,6 +359,8 @@ def run_ours(args):
 
     def ctypes_ptr(ev):
         return ev.cuda_event
+
+    use_graph = args.graph and world == 1  # (NCCL collectives stay eager for N > 1)
 
     for _ in range(args.warmup):
         step(True)
@@ -413,7 +441,8 @@ def run_ours(args):
                        "seed": args.seed, "parallelism": f"row-blocks x{world}" if world > 1 else "single GPU",
                        "step": "cold: plan build (part histogram, placement, per-part vertex sort) + fused row "
                                "kernel (+ NCCL nnz allgather when N>1)",
-                       "l2": "512 MB buffer zeroed between timed steps (outside the timed windows)"},
+                       "l2": "512 MB buffer zeroed between timed steps (outside the timed windows)",
+                       "launch": "CUDA graph replay per step" if (args.graph and world == 1) else "eager launches"},
             "hbm_gbs_whole_step": ab_total / (total_ms / args.steps * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "kernel": "k_rows (fused element + sparse() row kernel)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,

@@ -1190,17 +1190,26 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const unsigned long lon
 }
 
 
-// Optional CUDA events recorded around the row kernel (bench.py's per-kernel roofline).
+// Optional CUDA events recorded around the row kernel (bench.py's per-kernel roofline).  Inside
+// a stream capture they become external event-record nodes, so a replayed graph times too.
 static thread_local cudaEvent_t g_timer_begin = nullptr, g_timer_end = nullptr;
+
+static int record_timer(cudaEvent_t ev, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    FA_CUDA(cudaStreamIsCapturing(st, &cs));
+    if (cs == cudaStreamCaptureStatusActive) FA_CUDA(cudaEventRecordWithFlags(ev, st, cudaEventRecordExternal));
+    else FA_CUDA(cudaEventRecord(ev, st));
+    return FA_OK;
+}
 
 template <int KIND>
 static int launch_rows(const RowsArgs& A, int64_t nbuckets, cudaStream_t st) {
     const size_t smem = rows_smem_bytes<KIND>();
     FA_CUDA(cudaFuncSetAttribute(k_rows<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    if (g_timer_begin) FA_CUDA(cudaEventRecord(g_timer_begin, st));
+    if (g_timer_begin && record_timer(g_timer_begin, st) != FA_OK) return FA_ERR_CUDA;
     k_rows<KIND><<<dim3(unsigned(nbuckets)), KindTraits<KIND>::THREADS, smem, st>>>(A);
     FA_LAUNCH_CHECK("k_rows");
-    if (g_timer_end) FA_CUDA(cudaEventRecord(g_timer_end, st));
+    if (g_timer_end && record_timer(g_timer_end, st) != FA_OK) return FA_ERR_CUDA;
     return FA_OK;
 }
 
