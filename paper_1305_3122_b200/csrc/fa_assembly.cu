@@ -208,6 +208,7 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
         for (int i = tid; i < P.nparts; i += PLACE_THREADS) {
             const unsigned c = row[i];
             s_gb[i] = c ? atomicAdd(&P.part_fill[i], c) : 0u;
+            s_cnt[i] = 0;
         }
     }
     // triangle ids of the next round are loaded while the current one is placed
@@ -219,7 +220,6 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
         if (k < kb1) load_tri_ids(P.me, k, nxt[t][0], nxt[t][1], nxt[t][2]);
     }
     for (int64_t r0 = kb0; r0 < kb1; r0 += PLACE_TRI) {
-        for (int i = tid; i < P.nparts; i += PLACE_THREADS) s_cnt[i] = 0;
         int cur[TPT][3];
 #pragma unroll
         for (int t = 0; t < TPT; ++t) {
@@ -287,7 +287,10 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
                          : "memory");
         }
         __syncthreads();
-        for (int i = tid; i < P.nparts; i += PLACE_THREADS) s_gb[i] += s_cnt[i];
+        for (int i = tid; i < P.nparts; i += PLACE_THREADS) {  // advance the cursors, reset the counts
+            s_gb[i] += s_cnt[i];
+            s_cnt[i] = 0;
+        }
     }
 }
 
