@@ -438,9 +438,34 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_cons
             P.sn2[off + i] = n2[j];
         }
     } else {
+        // in place in global memory (L2-resident region of this part): short lists are read
+        // into registers, ranked and written back permuted; long ones heap-sorted
+        __threadfence_block();
         for (int v = tid; v < PV; v += SORT_THREADS) {
             const unsigned st = v ? s_cur[v - 1] : 0u, d = s_cur[v] - st;
-            if (d > 1) sort_incidences(key + st, n1 + st, n2 + st, int(d));
+            if (d <= 1) continue;
+            if (d <= 8) {
+                unsigned kk[8], a1[8], a2[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    kk[j] = j < int(d) ? key[st + j] : 0xffffffffu;
+                    a1[j] = j < int(d) ? n1[st + j] : 0u;
+                    a2[j] = j < int(d) ? n2[st + j] : 0u;
+                }
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    if (i < int(d)) {
+                        unsigned r = 0;
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) r += kk[j] < kk[i] ? 1u : 0u;
+                        key[st + r] = kk[i];
+                        n1[st + r] = a1[i];
+                        n2[st + r] = a2[i];
+                    }
+                }
+            } else {
+                sort_incidences(key + st, n1 + st, n2 + st, int(d));
+            }
         }
     }
 }

@@ -1,7 +1,7 @@
 #!/bin/bash
 # per-kernel durations of one cold C2 step (ncu launch list): tools/launch_list.sh OUT.csv [CFG]
 cfg=${2:-C2}
-ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__warps_active.avg.pct_of_peak_sustained_active,lts__t_sector_hit_rate.pct --clock-control none --print-units base --csv --log-file "$1" \
+ncu --metrics ${METRICS:-gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,sm__warps_active.avg.pct_of_peak_sustained_active,lts__t_sector_hit_rate.pct} --clock-control none --print-units base --csv --log-file "$1" \
   python -c "
 import sys; sys.argv=['x','$cfg']; sys.path.insert(0,'.')
 import tools.quick_time as q
