@@ -63,6 +63,8 @@ constexpr int SORT_THREADS = 512;   // k_part_sort (2 blocks / SM, 64 registers)
 constexpr int PLACE_THREADS = 1024;  // k_part_hist / k_part_place block size
 constexpr int PLACE_BLOCKS_PER_SM = 1;
 constexpr int PLACE_TRI = 2048;    // triangles per placement round
+constexpr int SPLIT_MIN = 8192;    // fine parts above which placement goes through coarse parts
+constexpr int SPLIT_COARSE = 1024; // coarse parts of a two-level plan (at most)
 constexpr int SORT_CAP = 7680;     // part incidences sorted in shared memory (2 blocks / SM)
 
 // Resets the result block and zeroes the counters the following kernels accumulate into
@@ -291,6 +293,106 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
             s_gb[i] += s_cnt[i];
             s_cnt[i] = 0;
         }
+    }
+}
+
+// K3b (two-level plans, row blocks above SPLIT_MIN fine parts): one block per coarse part, its
+// records regrouped by fine part (1024 vertices) into rec2 - counts in shared memory give the
+// fine part offsets (contiguous inside the coarse part's range), then rounds of records are
+// ranked, staged in fine-part order and written as coalesced runs.  The sort then works on
+// fine parts only, in shared memory.
+constexpr int SPLIT_THREADS = 1024;
+__global__ void __launch_bounds__(SPLIT_THREADS, 1)
+    k_part_split(const uint4* __restrict__ rec, const unsigned* __restrict__ part_off_c, int plog_c, int plog,
+                 unsigned* __restrict__ part_off_f, int64_t nparts_f, uint4* __restrict__ rec2) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int RI = 3 * PLACE_TRI;
+    constexpr int PER = RI / SPLIT_THREADS;
+    const int F = 1 << (plog_c - plog);  // fine parts per coarse part (<= 256)
+    uint4* s_stage = reinterpret_cast<uint4*>(smem_raw);          // [RI]
+    unsigned* s_cnt = reinterpret_cast<unsigned*>(s_stage + RI);  // [F]
+    unsigned* s_lst = s_cnt + F;                                  // [F]
+    unsigned* s_cur = s_lst + F;                                  // [F] global cursors
+    unsigned char* s_fp = reinterpret_cast<unsigned char*>(s_cur + F);  // [RI]
+    const int tid = threadIdx.x;
+    const int64_t pc = blockIdx.x;
+    const unsigned off = part_off_c[pc], n = part_off_c[pc + 1] - off;
+    const unsigned fmask = (1u << plog) - 1;
+    for (int f = tid; f < F; f += SPLIT_THREADS) s_cnt[f] = 0;
+    __syncthreads();
+    {
+        const unsigned* ry = reinterpret_cast<const unsigned*>(rec + off) + 1;
+        for (unsigned i0 = tid; i0 < n; i0 += 8 * SPLIT_THREADS) {
+            unsigned y[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const unsigned i = i0 + u * SPLIT_THREADS;
+                y[u] = i < n ? ry[4 * size_t(i)] : 0xffffffffu;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u)
+                if (y[u] != 0xffffffffu) atomicAdd(&s_cnt[(y[u] >> 2) >> plog], 1u);
+        }
+    }
+    __syncthreads();
+    if (tid == 0) {
+        unsigned run = 0;
+        for (int f = 0; f < F; ++f) {
+            const int64_t gf = (pc << (plog_c - plog)) + f;
+            s_cur[f] = off + run;
+            if (gf < nparts_f) part_off_f[gf] = off + run;
+            run += s_cnt[f];
+            s_cnt[f] = 0;
+        }
+        if (pc == int64_t(gridDim.x) - 1) part_off_f[nparts_f] = off + n;
+    }
+    __syncthreads();
+    for (unsigned r0 = 0; r0 < n; r0 += RI) {
+        uint4 r[PER];
+        unsigned fp[PER], rank[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const unsigned i = r0 + u * SPLIT_THREADS + tid;
+            fp[u] = 0xffffffffu;
+            if (i < n) {
+                r[u] = rec[off + i];
+                const unsigned vp = r[u].y >> 2;
+                fp[u] = vp >> plog;
+                rank[u] = atomicAdd(&s_cnt[fp[u]], 1u);
+                r[u].y = ((vp & fmask) << 2) | (r[u].y & 3u);
+            }
+        }
+        __syncthreads();
+        if (tid < 32) {  // local starts: exclusive scan of the round counts over the F fine parts
+            unsigned base = 0;
+            for (int f0 = 0; f0 < F; f0 += 32) {
+                const unsigned c = f0 + tid < F ? s_cnt[f0 + tid] : 0u;
+                const unsigned inc = warp_inclusive_scan(c);
+                if (f0 + tid < F) s_lst[f0 + tid] = base + inc - c;
+                base += __shfl_sync(0xffffffffu, inc, 31);
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            if (fp[u] != 0xffffffffu) {
+                const unsigned pos = s_lst[fp[u]] + rank[u];
+                s_stage[pos] = r[u];
+                s_fp[pos] = (unsigned char)fp[u];
+            }
+        }
+        __syncthreads();
+        const unsigned total = min(unsigned(RI), n - r0);
+        for (unsigned i = tid; i < total; i += SPLIT_THREADS) {
+            const unsigned f = s_fp[i];
+            rec2[s_cur[f] + (i - s_lst[f])] = s_stage[i];
+        }
+        __syncthreads();
+        for (int f = tid; f < F; f += SPLIT_THREADS) {
+            s_cur[f] += s_cnt[f];
+            s_cnt[f] = 0;
+        }
+        __syncthreads();
     }
 }
 
@@ -1250,13 +1352,17 @@ struct fa_plan {
     int device;
     int64_t nme, nq, v0, v1;
     int64_t nb;               // row buckets of BV vertices
-    int plog, nparts;
+    int plog, nparts;         // fine parts (sorted in shared memory)
+    int plog_c, nparts_c;     // placement parts (== fine unless two_level)
+    bool two_level;           // coarse placement + k_part_split (more than SPLIT_MIN fine parts)
     int64_t chunk_place;
     int nblk_place;
-    unsigned* part_off;       // nparts + 1
-    unsigned* part_fill;      // nparts
-    unsigned* M;              // [nblk_place][nparts]
-    uint4* rec;               // 3 * nme (owned incidences, grouped by part)
+    unsigned* part_off;       // nparts + 1 (fine)
+    unsigned* part_off_c;     // nparts_c + 1 (== part_off unless two_level)
+    unsigned* part_fill;      // nparts_c
+    unsigned* M;              // [nblk_place][nparts_c]
+    uint4* rec;               // 3 * nme (owned incidences, grouped by placement part)
+    uint4* rec2;              // two_level: regrouped by fine part
     unsigned* skey;           // 3 * nme
     unsigned* sn1;
     unsigned* sn2;
@@ -1277,7 +1383,8 @@ static void plan_free(fa_plan* p) {
     cudaFree(p->part_off); cudaFree(p->part_fill); cudaFree(p->M); cudaFree(p->rec); cudaFree(p->skey); cudaFree(p->sn1);
     cudaFree(p->sn2); cudaFree(p->ivptr); cudaFree(p->status);
     cudaFree(p->bsym); cudaFree(p->blen); cudaFree(p->bdrop); cudaFree(p->bshift); cudaFree(p->read_done);
-
+    if (p->part_off_c != p->part_off) cudaFree(p->part_off_c);
+    cudaFree(p->rec2);
 }
 
 static size_t place_smem_bytes(int nparts) {
@@ -1308,24 +1415,41 @@ extern "C" int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t ro
     p->nme = nme; p->nq = nq; p->v0 = row_begin; p->v1 = row_end;
     const int64_t nv = row_end - row_begin;
     p->nb = (nv + BV - 1) / BV;
+    // fine parts of 1024 vertices; test hook FEMASM_B200_PART_LOG2 forces larger ones (the
+    // sort's general global-memory path)
     p->plog = PLOG0;
-    while (((nv + (int64_t(1) << p->plog) - 1) >> p->plog) > MAX_PARTS) ++p->plog;
-    // test hook: FEMASM_B200_PART_LOG2 forces larger parts, i.e. the plan's general (global
-    // memory) sort path that very large row blocks take
     if (const char* env = getenv("FEMASM_B200_PART_LOG2")) {
         const int forced = atoi(env);
         if (forced > p->plog && forced <= 20) p->plog = forced;
     }
     p->nparts = int((nv + (int64_t(1) << p->plog) - 1) >> p->plog);
     if (p->nparts < 1) p->nparts = 1;
+    // placement coalesces runs of ~3 * PLACE_TRI / parts records: above SPLIT_MIN fine parts it
+    // works on coarse parts (<= SPLIT_COARSE of them) that k_part_split regroups
+    p->plog_c = p->plog;
+    p->two_level = p->nparts > SPLIT_MIN;
+    if (p->two_level)
+        while (((nv + (int64_t(1) << p->plog_c) - 1) >> p->plog_c) > SPLIT_COARSE) ++p->plog_c;
+    if (const char* env = getenv("FEMASM_B200_COARSE_LOG2")) {  // test hook: force a two-level plan
+        const int forced = atoi(env);
+        if (forced > p->plog && forced <= p->plog + 8) {
+            p->two_level = true;
+            p->plog_c = forced;
+        }
+    }
+    p->nparts_c = int((nv + (int64_t(1) << p->plog_c) - 1) >> p->plog_c);
+    if (p->nparts_c < 1) p->nparts_c = 1;
     p->chunk_place = (nme + PLACE_BLOCKS_PER_SM * NUM_SMS_B200 - 1) / (PLACE_BLOCKS_PER_SM * NUM_SMS_B200);
     p->nblk_place = int((nme + p->chunk_place - 1) / p->chunk_place);
     p->ninc = -1;
     const size_t ninc_max = size_t(3) * size_t(nme);
     cudaError_t e = cudaSuccess;
     if (e == cudaSuccess) e = cudaMalloc(&p->part_off, sizeof(unsigned) * (p->nparts + 1));
-    if (e == cudaSuccess) e = cudaMalloc(&p->part_fill, sizeof(unsigned) * p->nparts);
-    if (e == cudaSuccess) e = cudaMalloc(&p->M, sizeof(unsigned) * size_t(p->nblk_place) * p->nparts);
+    p->part_off_c = p->part_off;
+    if (e == cudaSuccess && p->two_level) e = cudaMalloc(&p->part_off_c, sizeof(unsigned) * (p->nparts_c + 1));
+    if (e == cudaSuccess && p->two_level) e = cudaMalloc(&p->rec2, sizeof(uint4) * ninc_max);
+    if (e == cudaSuccess) e = cudaMalloc(&p->part_fill, sizeof(unsigned) * p->nparts_c);
+    if (e == cudaSuccess) e = cudaMalloc(&p->M, sizeof(unsigned) * size_t(p->nblk_place) * p->nparts_c);
     if (e == cudaSuccess) e = cudaMalloc(&p->rec, sizeof(uint4) * ninc_max);
     if (e == cudaSuccess) e = cudaMalloc(&p->skey, sizeof(unsigned) * ninc_max);
     if (e == cudaSuccess) e = cudaMalloc(&p->sn1, sizeof(unsigned) * ninc_max);
@@ -1365,23 +1489,33 @@ extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, 
         k_reset_result<<<1, 32, 0, st>>>(d_res);
         return FA_OK;
     }
-    k_reset<<<4, 256, 0, st>>>(d_res, p->part_off, p->nparts + 1, nullptr, 0);  // result + part counts
+    k_reset<<<4, 256, 0, st>>>(d_res, p->part_off_c, p->nparts_c + 1, nullptr, 0);  // result + part counts
     FA_LAUNCH_CHECK("k_reset");
-    PlanArgs P;
+    PlanArgs P;  // placement level (coarse parts when two_level)
     P.me = d_me; P.nme = p->nme; P.nq = p->nq; P.v0 = p->v0; P.v1 = p->v1;
-    P.plog = p->plog; P.nparts = p->nparts; P.chunk = p->chunk_place;
-    P.part_off = p->part_off; P.part_fill = p->part_fill; P.M = p->M; P.rec = p->rec;
+    P.plog = p->plog_c; P.nparts = p->nparts_c; P.chunk = p->chunk_place;
+    P.part_off = p->part_off_c; P.part_fill = p->part_fill; P.M = p->M; P.rec = p->rec;
     P.skey = p->skey; P.sn1 = p->sn1; P.sn2 = p->sn2; P.ivptr = p->ivptr; P.res = d_res;
-    const size_t hist_smem = sizeof(unsigned) * p->nparts;
+    const size_t hist_smem = sizeof(unsigned) * p->nparts_c;
     FA_CUDA(cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_smem)));
     k_part_hist<<<p->nblk_place, PLACE_THREADS, hist_smem, st>>>(P);
     FA_LAUNCH_CHECK("k_part_hist");
     k_part_scan<<<1, PLAN_THREADS, 0, st>>>(P);
     FA_LAUNCH_CHECK("k_part_scan");
-    const size_t place_smem = place_smem_bytes(p->nparts);
+    const size_t place_smem = place_smem_bytes(p->nparts_c);
     FA_CUDA(cudaFuncSetAttribute(k_part_place, cudaFuncAttributeMaxDynamicSharedMemorySize, int(place_smem)));
     k_part_place<<<p->nblk_place, PLACE_THREADS, place_smem, st>>>(P);
     FA_LAUNCH_CHECK("k_part_place");
+    if (p->two_level) {
+        const int F = 1 << (p->plog_c - p->plog);
+        const size_t split_smem = size_t(3 * PLACE_TRI) * (sizeof(uint4) + 1) + sizeof(unsigned) * 3 * F;
+        FA_CUDA(cudaFuncSetAttribute(k_part_split, cudaFuncAttributeMaxDynamicSharedMemorySize, int(split_smem)));
+        k_part_split<<<p->nparts_c, SPLIT_THREADS, split_smem, st>>>(p->rec, p->part_off_c, p->plog_c, p->plog,
+                                                                       p->part_off, p->nparts, p->rec2);
+        FA_LAUNCH_CHECK("k_part_split");
+    }
+    P.plog = p->plog; P.nparts = p->nparts; P.part_off = p->part_off;  // sort level: fine parts
+    P.rec = p->two_level ? p->rec2 : p->rec;
     const size_t sort_smem = sort_smem_bytes(p->plog);
     FA_CUDA(cudaFuncSetAttribute(k_part_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sort_smem)));
     k_part_sort<<<p->nparts, SORT_THREADS, sort_smem, st>>>(P);

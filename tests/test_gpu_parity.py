@@ -247,3 +247,21 @@ def test_isolated_vertices_have_empty_rows():
         ref = c_oracle.assemble(kind, V, C, areas, w, 1.0, 0.5)
         got, _ = plan_assemble(kind, V, C, areas, w, 1.0, 0.5)
         assert_same_csc(got, ref, kind)
+
+
+@pytest.mark.parametrize("coarse_log2", (11, 14))
+@pytest.mark.parametrize("kind", KINDS)
+def test_two_level_plan(monkeypatch, kind, coarse_log2):
+    """Row blocks above 8192 fine parts place incidences by coarse part and regroup them
+    (k_part_split); forced here on a small mesh and checked bitwise."""
+    monkeypatch.setenv("FEMASM_B200_COARSE_LOG2", str(coarse_log2))
+    sm = seeded_square_mesh(70, 4)  # 5041 vertices: 5 fine parts
+    areas = fo.triangle_areas(sm.vertices, sm.connectivity)
+    ref = c_oracle.assemble(kind, sm.vertices, sm.connectivity, areas, sm.weights, 1.5, 0.6)
+    got, _ = plan_assemble(kind, sm.vertices, sm.connectivity, areas, sm.weights, 1.5, 0.6)
+    assert_same_csc(got, ref, f"{kind} coarse_log2={coarse_log2}")
+    blocks = [(0, 1700), (1700, 3500), (3500, sm.nq)]
+    for v0, v1 in blocks:  # row blocks too
+        got, _ = plan_assemble(kind, sm.vertices, sm.connectivity, areas, sm.weights, 1.5, 0.6, v0=v0, v1=v1)
+        sub = fo.assemble_row_block(kind, sm.vertices, sm.connectivity, areas, sm.weights, 1.5, 0.6, v0, v1)
+        assert_same_csc(got, sub, f"{kind} block {v0}:{v1}")
