@@ -50,7 +50,10 @@
 
 namespace fa {
 
-constexpr int BV = 128;            // vertices per row bucket
+#ifndef FA_BV
+#define FA_BV 128
+#endif
+constexpr int BV = FA_BV;          // vertices per row bucket
 #ifndef FA_CAPB
 #define FA_CAPB (8 * BV)
 #endif
