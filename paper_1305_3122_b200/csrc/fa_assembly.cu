@@ -11,29 +11,38 @@
 // pass needs except floating-point data, so the numeric pass gathers only from the small,
 // L2-resident arrays (areas 8 B/triangle, q 16 B/vertex, w 8 B/vertex):
 //   plan (symbolic, reads `me` only)
-//     K1 part_hist   owned incidences per part (PV consecutive vertices) - shared-memory
-//                    histogram, one global atomic per (block, part)
+//     K1 part_hist   owned incidences per (block, part) (parts = 1024 consecutive vertices)
+//                    in shared memory, and per part; index validation
 //     K2 part_scan   part offsets
 //     K3 part_place  per round of triangles: incidence records {k, vertex-in-part<<2|a, n1, n2}
-//                    ranked by part in shared memory, one range reserved per (round, part),
-//                    written as coalesced runs
+//                    ranked by part in shared memory, one range per (block, part) reserved once,
+//                    staged in part order and written as coalesced runs
+//     K3b part_split (two-level plans only: more than SPLIT_MIN parts) placement used coarse
+//                    parts; one block per coarse part regroups its records by fine part
 //     K4 part_sort   per part: counting sort by vertex in shared memory, each vertex's list
-//                    sorted by k; written as SoA (k<<2|a, n1, n2) + per-vertex offsets ivptr
+//                    ordered by k; written as SoA (k<<2|a, n1, n2) + per-vertex offsets ivptr
 //   numeric
-//     K5 rows        one block per bucket of BV vertices:
-//                    a) per incidence (balanced over threads): plan entry (coalesced), the
-//                       triangle area and neighbour q / w (gathers from L2-resident arrays),
-//                       the row of the element matrix computed bit-exactly into shared memory
-//                       (gradients + area for elasticity);
-//                    c) one thread per matrix row: its <= MAXD incidences are contiguous and in
-//                       ascending k; the 2*deg neighbour columns are sorted with a 16-key
-//                       odd-even merge network; a linear pass sums every position sequentially
-//                       in ascending k (== stable argsort + bincount of the reference) and
-//                       drops exact-zero sums;
-//                    d) block scan + decoupled look-back for the global row offset; the
-//                       bucket's CSR segment is staged in shared memory and written coalesced.
+//     K5 rows        one block per bucket of BV vertices, ticket-ordered:
+//                    s) plan entries into shared memory in one round trip; per row the 2*deg
+//                       neighbour columns sorted with a 16-key odd-even merge network -> the
+//                       row's symbolic entry count; block scan; for the scalar kinds the
+//                       bucket's size is published to the decoupled look-back right away;
+//                    a) per incidence (balanced over threads): the triangle area and the
+//                       neighbour q / w gathered (L2-resident arrays, evict-last), the row of
+//                       the element matrix computed bit-exactly into shared memory (gradients
+//                       + area for elasticity);
+//                    c) one thread per matrix row: a linear pass over the sorted columns sums
+//                       every position sequentially in ascending k (== stable argsort +
+//                       bincount of the reference); exact-zero sums stay as entries (scalar
+//                       kinds) or are dropped at once (elasticity, which then publishes its
+//                       exact count);
+//                    d) the bucket's CSR segment staged in shared memory, look-back resolved,
+//                       written coalesced.
+//     K6 compact     only when a scalar-kind sum was exactly zero (Matlab drops it,
+//                    sparse.py:177-179): removes those entries in place, bucket by bucket.
 // Rows of degree > MAXD (and every row of a bucket whose incidences exceed CAPB) use an
-// O(d^2) general path with the same summation order.
+// O(d^2) general path with the same summation order.  Build-time knobs (experiments):
+// FA_ROWS_AU, FA_ROWS_MINB, FA_CAPB, FA_BV; FA_EXP_TIMELINE records per-block phase times.
 #include <climits>
 #include <cstdlib>
 #include <new>
