@@ -58,7 +58,7 @@ typedef struct fa_result {
     int64_t col_error_pos;     /* first out-of-range column index position (triplets)      */
     int64_t dropped;           /* positions dropped because their sum was exactly 0.0     */
     int64_t heavy_rows;        /* rows that took the general (degree > 8) path             */
-    int64_t reserved[2];
+    int64_t reserved[2];       /* internal: [0] exact zeros left for the in-place compaction */
 } fa_result;
 
 /* Map a HOST copy of an fa_result block to a status code (FA_OK when clean). */
@@ -81,8 +81,10 @@ typedef struct fa_plan fa_plan;
 int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t row_begin, int64_t row_end);
 
 /* (Re)build the incidence structure from connectivity d_me (nme x 3 int32, row-major,
- * 0-based).  Asynchronous on `stream`; d_me must stay valid and unchanged until the next
- * fa_plan_build or fa_plan_destroy.  Out-of-range vertex ids are reported in d_result. */
+ * 0-based): every owned vertex's (triangle, corner, neighbours) list, sorted by triangle.
+ * Asynchronous on `stream`; d_me is read only by the kernels of this call (the plan keeps
+ * its own copy of what the numeric pass needs).  Out-of-range vertex ids are reported in
+ * d_result. */
 int fa_plan_build(fa_plan* plan, const int32_t* d_me, fa_result* d_result, void* stream);
 
 /* Upper bound on stored entries for `kind` over the plan's rows (capacity of d_col/d_val):
@@ -108,6 +110,7 @@ int fa_plan_destroy(fa_plan* plan);
  *            compute_areas' formula (mesh.py:62-65) - only valid for areas produced by it
  *   d_w      (nq) f64 vertex weights (MASSW only; WeightField.sample, assembly.py:114)
  *   lam, mu  Lame parameters (ELASTIC only; ElasticParams, elements.py:81-103)
+ * Exact-zero sums are dropped (sparse.py:177-179) and counted in d_result->dropped.
  * Capacity must be >= fa_plan_capacity(kind).  Asynchronous. */
 int fa_assemble(fa_plan* plan, int kind, const double* d_q, const double* d_areas,
                 const double* d_w, double lam, double mu, int64_t* d_rowptr, int32_t* d_col,
