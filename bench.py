@@ -40,7 +40,7 @@ METRIC = "triangles assembled/sec (device-timed, incl. CSR build)"
 UNIT = "triangles/s"
 # our kernels launched per cold step (fa_plan_build + fa_assemble); memsets are not counted
 LAUNCHES_PER_STEP = ["k_reset", "k_part_hist", "k_part_scan", "k_part_place", "k_part_sort",
-                     "k_reset", "k_rows", "k_compact (exits at once unless a sum was exactly zero)"]
+                     "k_reset", "k_tri_wt (weighted mass)", "k_rows", "k_compact (exits at once unless a sum was exactly zero)"]
 DEFAULT_CONFIG = "C2"
 DESCR = {
     "C1": "P1 mass, N=256 seeded jittered/permuted unit square",

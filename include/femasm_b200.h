@@ -82,9 +82,9 @@ int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t row_begin, in
 
 /* (Re)build the incidence structure from connectivity d_me (nme x 3 int32, row-major,
  * 0-based): every owned vertex's (triangle, corner, neighbours) list, sorted by triangle.
- * Asynchronous on `stream`; d_me is read only by the kernels of this call (the plan keeps
- * its own copy of what the numeric pass needs).  Out-of-range vertex ids are reported in
- * d_result. */
+ * Asynchronous on `stream`; d_me must stay valid and unchanged until the next
+ * fa_plan_build or fa_plan_destroy (the weighted-mass numeric pass reads it once per
+ * triangle).  Out-of-range vertex ids are reported in d_result. */
 int fa_plan_build(fa_plan* plan, const int32_t* d_me, fa_result* d_result, void* stream);
 
 /* Upper bound on stored entries for `kind` over the plan's rows (capacity of d_col/d_val):
@@ -107,7 +107,8 @@ int fa_plan_destroy(fa_plan* plan);
  * bit for bit.
  *   d_q      (nq x 2) f64 vertex coordinates (STIFF, ELASTIC; may be NULL for MASS, MASSW)
  *   d_areas  (nme) f64 triangle areas, or NULL to recompute them bitwise from d_q with
- *            compute_areas' formula (mesh.py:62-65) - only valid for areas produced by it
+ *            compute_areas' formula (mesh.py:62-65) - only valid for areas produced by it;
+ *            required for MASSW
  *   d_w      (nq) f64 vertex weights (MASSW only; WeightField.sample, assembly.py:114)
  *   lam, mu  Lame parameters (ELASTIC only; ElasticParams, elements.py:81-103)
  * Exact-zero sums are dropped (sparse.py:177-179) and counted in d_result->dropped.

@@ -608,6 +608,7 @@ struct RowsArgs {
     unsigned* blen;         // per bucket: symbolic length
     unsigned* bdrop;        // per bucket: entries that summed to exactly zero
     unsigned* read_done;    // per bucket: k_compact flag, zeroed here
+    const double4* Wt;      // weighted mass: per-triangle W0..W2 (k_tri_wt)
     fa_result* res;
 };
 
@@ -633,6 +634,7 @@ constexpr size_t rows_smem_bytes() {
 struct Gathered {
     double2 p1, p2;
     double w1, w2, ar;
+    double4 wt;  // weighted mass: the triangle's W0, W1, W2 (k_tri_wt)
 };
 
 template <int KIND>
@@ -646,15 +648,15 @@ __device__ __forceinline__ Gathered gather_incidence(const RowsArgs& A, unsigned
 #endif
     g.p1 = g.p2 = make_double2(0.0, 0.0);
     g.w1 = g.w2 = 0.0;
-    g.ar = A.areas ? ld_keep_f64(A.areas + k, pol) : 0.0;
+    g.ar = (KIND != FA_KIND_MASSW && A.areas) ? ld_keep_f64(A.areas + k, pol) : 0.0;
     if (KIND == FA_KIND_STIFF || KIND == FA_KIND_ELASTIC || !A.areas) {
         g.p1 = ld_keep_f64x2(A.q + n1, pol);
         g.p2 = ld_keep_f64x2(A.q + n2, pol);
     }
-    if (KIND == FA_KIND_MASSW) {
-        g.w1 = ld_keep_f64(A.w + n1, pol);
-        g.w2 = ld_keep_f64(A.w + n2, pol);
-    }
+    if (KIND == FA_KIND_MASSW)  // the triangle's three W (k_tri_wt): one 32-byte gather
+        asm volatile("ld.global.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+                     : "=d"(g.wt.x), "=d"(g.wt.y), "=d"(g.wt.z), "=d"(g.wt.w)
+                     : "l"(A.Wt + k), "l"(pol));
     return g;
 }
 
@@ -679,10 +681,9 @@ __device__ __forceinline__ void incidence_values(const RowsArgs& A, unsigned k, 
         out[1] = m.o;
         out[2] = m.o;
     } else if constexpr (KIND == FA_KIND_MASSW) {
-        // W of the own corner and of the corners a+1 (n1), a+2 (n2): assembly.py:232-234
-        const double Wo = ddiv_rcp(FMUL(own_w, ar), 30.0, FA_RCP30);
-        const double W1 = ddiv_rcp(FMUL(g.w1, ar), 30.0, FA_RCP30);
-        const double W2 = ddiv_rcp(FMUL(g.w2, ar), 30.0, FA_RCP30);
+        // W of the own corner a and of the corners a+1 (n1), a+2 (n2) (k_tri_wt)
+        const double Wo = sel3(a, g.wt.x, g.wt.y, g.wt.z), W1 = sel3(a, g.wt.y, g.wt.z, g.wt.x),
+                     W2 = sel3(a, g.wt.z, g.wt.x, g.wt.y);
         // row a of assembly.py:236-241 in the triangle's corner order (additions are not
         // associative, so each corner keeps its own formula):
         //   a=0: diag (3*W0 + W1) + W2,  (0,1) (W0 + W1) + W2/2,  (0,2) (W0 + W1/2) + W2
@@ -908,7 +909,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     for (int i = tid; i < BV; i += NT) {
         const int64_t vv = vbase + i;
         s_oq[i] = (A.q && vv < A.v1) ? A.q[vv] : make_double2(0.0, 0.0);
-        s_ow[i] = (KIND == FA_KIND_MASSW && vv < A.v1) ? A.w[vv] : 0.0;
+        s_ow[i] = 0.0;  // (the weighted mass reads its W per triangle, k_tri_wt)
     }
     __syncthreads();
     const bool overflow = s_vst[BV] > CAPB;
@@ -1332,6 +1333,28 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const unsigned long lon
 }
 
 
+// Weighted mass: W_c = (w[me[k,c]] * area_k) / 30 for the three corners, once per triangle
+// (assembly.py:232-234), coalesced; the row kernel gathers one 32-byte record per incidence.
+__global__ void k_tri_wt(const int32_t* __restrict__ me, int64_t nme, const double* __restrict__ areas,
+                         const double* __restrict__ w, double4* __restrict__ Wt) {
+    const uint64_t pol = l2_evict_first_policy();
+    const uint64_t keep = l2_evict_last_policy();
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nme; k += int64_t(gridDim.x) * blockDim.x) {
+        const int c0 = ld_stream_i32(me + 3 * k, pol), c1 = ld_stream_i32(me + 3 * k + 1, pol),
+                  c2 = ld_stream_i32(me + 3 * k + 2, pol);
+        const double ar = ld_stream_f64(areas + k, pol);
+        const double w0 = ld_keep_f64(w + c0, keep), w1 = ld_keep_f64(w + c1, keep), w2 = ld_keep_f64(w + c2, keep);
+        double4 r;
+        r.x = ddiv_rcp(FMUL(w0, ar), 30.0, FA_RCP30);
+        r.y = ddiv_rcp(FMUL(w1, ar), 30.0, FA_RCP30);
+        r.z = ddiv_rcp(FMUL(w2, ar), 30.0, FA_RCP30);
+        r.w = 0.0;
+        asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(Wt + k), "d"(r.x), "d"(r.y),
+                     "d"(r.z), "d"(r.w), "l"(keep)
+                     : "memory");
+    }
+}
+
 // Optional CUDA events recorded around the row kernel (bench.py's per-kernel roofline).  Inside
 // a stream capture they become external event-record nodes, so a replayed graph times too.
 static thread_local cudaEvent_t g_timer_begin = nullptr, g_timer_end = nullptr;
@@ -1375,6 +1398,8 @@ struct fa_plan {
     unsigned* M;              // [nblk_place][nparts_c]
     uint4* rec;               // 3 * nme (owned incidences, grouped by placement part)
     uint4* rec2;              // two_level: regrouped by fine part
+    const int32_t* me;        // connectivity of the last build (caller keeps it: weighted mass)
+    double4* Wt;              // weighted mass: per-triangle W records (allocated on first use)
     unsigned* skey;           // 3 * nme
     unsigned* sn1;
     unsigned* sn2;
@@ -1397,6 +1422,7 @@ static void plan_free(fa_plan* p) {
     cudaFree(p->bsym); cudaFree(p->blen); cudaFree(p->bdrop); cudaFree(p->bshift); cudaFree(p->read_done);
     if (p->part_off_c != p->part_off) cudaFree(p->part_off_c);
     cudaFree(p->rec2);
+    cudaFree(p->Wt);
 }
 
 static size_t place_smem_bytes(int nparts) {
@@ -1501,6 +1527,7 @@ extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, 
         k_reset_result<<<1, 32, 0, st>>>(d_res);
         return FA_OK;
     }
+    p->me = d_me;
     k_reset<<<4, 256, 0, st>>>(d_res, p->part_off_c, p->nparts_c + 1, nullptr, 0);  // result + part counts
     FA_LAUNCH_CHECK("k_reset");
     PlanArgs P;  // placement level (coarse parts when two_level)
@@ -1603,6 +1630,14 @@ extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double
     A.status = p->status; A.ticket = reinterpret_cast<unsigned long long*>(p->status + p->nb); A.res = d_res;
     A.read_done = p->read_done;
     A.bsym = p->bsym; A.blen = p->blen; A.bdrop = p->bdrop;
+    A.Wt = nullptr;
+    if (kind == FA_KIND_MASSW) {  // the triangles' W once (k_tri_wt), gathered per incidence
+        if (!d_areas) { set_error("WEIGHTED_MASS requires areas"); return FA_ERR_ARGUMENT; }
+        if (!p->Wt) FA_CUDA(cudaMalloc(&p->Wt, sizeof(double4) * size_t(p->nme)));
+        k_tri_wt<<<unsigned((p->nme + 255) / 256), 256, 0, st>>>(p->me, p->nme, d_areas, d_w, p->Wt);
+        FA_LAUNCH_CHECK("k_tri_wt");
+        A.Wt = p->Wt;
+    }
     int rc;
     switch (kind) {
         case FA_KIND_MASS: rc = launch_rows<FA_KIND_MASS>(A, p->nb, st); break;

@@ -38,7 +38,7 @@ class AssemblyPlan:
 
     def build(self, me_dev, stream=None) -> None:
         """(Re)build the incidence structure from device connectivity (nme, 3) int32."""
-        self._me = me_dev  # keep alive until the (asynchronous) build has read it
+        self._me = me_dev  # keep alive: the weighted-mass numeric pass reads it (fa_plan_build contract)
         self._capacity.clear()
         rc = _lib.lib().fa_plan_build(self._h, me_dev.data_ptr(), self._build_res.ptr, _lib.stream_handle(stream))
         _lib.check(rc, "fa_plan_build")
