@@ -1335,23 +1335,43 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const unsigned long lon
 
 // Weighted mass: W_c = (w[me[k,c]] * area_k) / 30 for the three corners, once per triangle
 // (assembly.py:232-234), coalesced; the row kernel gathers one 32-byte record per incidence.
-__global__ void k_tri_wt(const int32_t* __restrict__ me, int64_t nme, const double* __restrict__ areas,
-                         const double* __restrict__ w, double4* __restrict__ Wt) {
+constexpr int TRI_WT_U = 4;  // triangles in flight per thread
+__global__ void __launch_bounds__(256) k_tri_wt(const int32_t* __restrict__ me, int64_t nme,
+                                                 const double* __restrict__ areas, const double* __restrict__ w,
+                                                 double4* __restrict__ Wt) {
     const uint64_t pol = l2_evict_first_policy();
     const uint64_t keep = l2_evict_last_policy();
-    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nme; k += int64_t(gridDim.x) * blockDim.x) {
-        const int c0 = ld_stream_i32(me + 3 * k, pol), c1 = ld_stream_i32(me + 3 * k + 1, pol),
-                  c2 = ld_stream_i32(me + 3 * k + 2, pol);
-        const double ar = ld_stream_f64(areas + k, pol);
-        const double w0 = ld_keep_f64(w + c0, keep), w1 = ld_keep_f64(w + c1, keep), w2 = ld_keep_f64(w + c2, keep);
-        double4 r;
-        r.x = ddiv_rcp(FMUL(w0, ar), 30.0, FA_RCP30);
-        r.y = ddiv_rcp(FMUL(w1, ar), 30.0, FA_RCP30);
-        r.z = ddiv_rcp(FMUL(w2, ar), 30.0, FA_RCP30);
-        r.w = 0.0;
-        asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(Wt + k), "d"(r.x), "d"(r.y),
-                     "d"(r.z), "d"(r.w), "l"(keep)
-                     : "memory");
+    const int64_t k0 = int64_t(blockIdx.x) * (256 * TRI_WT_U) + threadIdx.x;
+    int c[TRI_WT_U][3];
+    double ar[TRI_WT_U], wc[TRI_WT_U][3];
+#pragma unroll
+    for (int u = 0; u < TRI_WT_U; ++u) {
+        const int64_t k = k0 + u * 256;
+        if (k < nme) {
+            c[u][0] = ld_stream_i32(me + 3 * k, pol);
+            c[u][1] = ld_stream_i32(me + 3 * k + 1, pol);
+            c[u][2] = ld_stream_i32(me + 3 * k + 2, pol);
+            ar[u] = ld_stream_f64(areas + k, pol);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < TRI_WT_U; ++u)
+        if (k0 + u * 256 < nme)
+#pragma unroll
+            for (int a = 0; a < 3; ++a) wc[u][a] = ld_keep_f64(w + c[u][a], keep);
+#pragma unroll
+    for (int u = 0; u < TRI_WT_U; ++u) {
+        const int64_t k = k0 + u * 256;
+        if (k < nme) {
+            double4 r;
+            r.x = ddiv_rcp(FMUL(wc[u][0], ar[u]), 30.0, FA_RCP30);
+            r.y = ddiv_rcp(FMUL(wc[u][1], ar[u]), 30.0, FA_RCP30);
+            r.z = ddiv_rcp(FMUL(wc[u][2], ar[u]), 30.0, FA_RCP30);
+            r.w = 0.0;
+            asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(Wt + k), "d"(r.x),
+                         "d"(r.y), "d"(r.z), "d"(r.w), "l"(keep)
+                         : "memory");
+        }
     }
 }
 
@@ -1634,7 +1654,8 @@ extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double
     if (kind == FA_KIND_MASSW) {  // the triangles' W once (k_tri_wt), gathered per incidence
         if (!d_areas) { set_error("WEIGHTED_MASS requires areas"); return FA_ERR_ARGUMENT; }
         if (!p->Wt) FA_CUDA(cudaMalloc(&p->Wt, sizeof(double4) * size_t(p->nme)));
-        k_tri_wt<<<unsigned((p->nme + 255) / 256), 256, 0, st>>>(p->me, p->nme, d_areas, d_w, p->Wt);
+        k_tri_wt<<<unsigned((p->nme + 256 * TRI_WT_U - 1) / (256 * TRI_WT_U)), 256, 0, st>>>(p->me, p->nme, d_areas,
+                                                                                           d_w, p->Wt);
         FA_LAUNCH_CHECK("k_tri_wt");
         A.Wt = p->Wt;
     }
