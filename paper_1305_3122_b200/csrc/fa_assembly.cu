@@ -1335,7 +1335,10 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const unsigned long lon
 
 // Weighted mass: W_c = (w[me[k,c]] * area_k) / 30 for the three corners, once per triangle
 // (assembly.py:232-234), coalesced; the row kernel gathers one 32-byte record per incidence.
-constexpr int TRI_WT_U = 4;  // triangles in flight per thread
+#ifndef FA_TRI_WT_U
+#define FA_TRI_WT_U 4
+#endif
+constexpr int TRI_WT_U = FA_TRI_WT_U;  // triangles in flight per thread
 __global__ void __launch_bounds__(256) k_tri_wt(const int32_t* __restrict__ me, int64_t nme,
                                                  const double* __restrict__ areas, const double* __restrict__ w,
                                                  double4* __restrict__ Wt) {
