@@ -50,6 +50,12 @@
 #include "fa_common.cuh"
 #include "fa_element.cuh"
 
+#ifndef FA_ROWS_MINB_E
+#define FA_ROWS_MINB_E 2
+#endif
+#ifndef FA_ROWS_AU_E
+#define FA_ROWS_AU_E 1  // elasticity (12 values per incidence)
+#endif
 #ifndef FA_ROWS_AU
 #define FA_ROWS_AU 4  // incidences in flight per thread in the row kernel phase a
 #endif
@@ -63,6 +69,9 @@ namespace fa {
 #define FA_BV 128
 #endif
 constexpr int BV = FA_BV;          // vertices per row bucket
+#ifndef FA_CAPB_E
+#define FA_CAPB_E (7 * BV)  // elasticity: 12 values per incidence, two blocks per SM
+#endif
 #ifndef FA_CAPB
 #define FA_CAPB (8 * BV)
 #endif
@@ -617,11 +626,12 @@ struct KindTraits {
     static constexpr int RPV = KIND == FA_KIND_ELASTIC ? 2 : 1;  // rows per vertex
     static constexpr int NV = KIND == FA_KIND_ELASTIC ? 2 : 1;   // values per (row, vertex column)
     static constexpr int THREADS = BV * RPV;
-    // per-record shared data: scalar kinds store the row's three values, elasticity the
-    // triangle's gradients + area (entries are formed per dof row in the merge)
-    static constexpr int RVALS = KIND == FA_KIND_ELASTIC ? 7 : 3;
-    static constexpr int MIN_BLOCKS = KIND == FA_KIND_ELASTIC ? 2 : FA_ROWS_MINB;
-    static constexpr size_t REC_BYTES = size_t(CAPB) * (RVALS * 8 + 12);
+    // per-record shared data: scalar kinds store the row's three values, elasticity the 2 x 6
+    // entries of its two dof rows (own, n1, n2 vertex columns, x and y)
+    static constexpr int RVALS = KIND == FA_KIND_ELASTIC ? 12 : 3;
+    static constexpr int MIN_BLOCKS = KIND == FA_KIND_ELASTIC ? FA_ROWS_MINB_E : FA_ROWS_MINB;
+    static constexpr int CAP = KIND == FA_KIND_ELASTIC ? FA_CAPB_E : CAPB;  // incidences in shared memory
+    static constexpr size_t REC_BYTES = size_t(CAP) * (RVALS * 8 + 12);
     static constexpr int STAGE = int(REC_BYTES / 12);  // staged entries fitting the records area
 };
 
@@ -706,10 +716,15 @@ __device__ __forceinline__ void incidence_values(const RowsArgs& A, unsigned k, 
         out[2] = stiff_entry(m, a, b2);
     } else {
         const ElasticTri m = elastic_prepare(c0, c1, c2, ar);
-        out[0] = m.g0.x; out[1] = m.g0.y;
-        out[2] = m.g1.x; out[3] = m.g1.y;
-        out[4] = m.g2.x; out[5] = m.g2.y;
-        out[6] = m.area;
+        const double P = FADD(A.lam, FMUL(2.0, A.mu));
+#pragma unroll
+        for (int s = 0; s < 2; ++s)
+#pragma unroll
+            for (int rel = 0; rel < 3; ++rel) {
+                const int bl = rel == 0 ? a : (rel == 1 ? (a == 2 ? 0 : a + 1) : (a == 0 ? 2 : a - 1));
+#pragma unroll
+                for (int t = 0; t < 2; ++t) out[s * 6 + rel * 2 + t] = elastic_entry(m, 2 * a + s, 2 * bl + t, A.lam, A.mu, P);
+            }
     }
 }
 
@@ -718,14 +733,7 @@ __device__ __forceinline__ void incidence_values(const RowsArgs& A, unsigned k, 
 template <int KIND>
 __device__ __forceinline__ double entry_from(const RowsArgs& A, const double* rv, int a, int s, int rel, int t) {
     if constexpr (KIND == FA_KIND_ELASTIC) {
-        ElasticTri m;
-        m.g0 = make_double2(rv[0], rv[1]);
-        m.g1 = make_double2(rv[2], rv[3]);
-        m.g2 = make_double2(rv[4], rv[5]);
-        m.area = rv[6];
-        const double P = FADD(A.lam, FMUL(2.0, A.mu));
-        const int bl = rel == 0 ? a : (rel == 1 ? (a == 2 ? 0 : a + 1) : (a == 0 ? 2 : a - 1));
-        return elastic_entry(m, 2 * a + s, 2 * bl + t, A.lam, A.mu, P);
+        return rv[s * 6 + rel * 2 + t];
     } else {
         return rel == 0 ? rv[0] : (rel == 1 ? rv[1] : rv[2]);
     }
@@ -735,13 +743,11 @@ __device__ __forceinline__ double entry_from(const RowsArgs& A, const double* rv
 template <int KIND>
 __device__ __forceinline__ double record_entry(const RowsArgs& A, const double* vals, int slot, int a, int s,
                                                int rel, int t) {
+    constexpr int CAP = KindTraits<KIND>::CAP;
     if constexpr (KIND == FA_KIND_ELASTIC) {
-        double rv[7];
-#pragma unroll
-        for (int j = 0; j < 7; ++j) rv[j] = vals[j * CAPB + slot];
-        return entry_from<KIND>(A, rv, a, s, rel, t);
+        return vals[(s * 6 + rel * 2 + t) * CAP + slot];
     } else {
-        return vals[rel * CAPB + slot];
+        return vals[rel * CAP + slot];
     }
 }
 
@@ -764,10 +770,10 @@ __device__ __forceinline__ void sort16(unsigned (&k)[16]) {
 
 // Shared records of one bucket.
 struct BucketRecs {
-    double* vals;          // [RVALS][CAPB]
-    int* n1;               // [CAPB]
-    int* n2;               // [CAPB]
-    unsigned* ka;          // [CAPB] k << 2 | local corner of the row's vertex
+    double* vals;          // [RVALS][CAP]
+    int* n1;               // [CAP]
+    int* n2;               // [CAP]
+    unsigned* ka;          // [CAP] k << 2 | local corner of the row's vertex
 };
 
 struct RowCount {
@@ -792,7 +798,7 @@ __device__ __noinline__ RowCount general_row(const RowsArgs& A, BucketRecs R, bo
             n1 = R.n1[slot];
             n2 = R.n2[slot];
             if (need_vals)
-                for (int j = 0; j < RVALS; ++j) rv[j] = R.vals[j * CAPB + slot];
+                for (int j = 0; j < RVALS; ++j) rv[j] = R.vals[j * KindTraits<KIND>::CAP + slot];
             return;
         }
         const unsigned ka = A.skey[gfirst + i];
@@ -824,7 +830,7 @@ __device__ __noinline__ RowCount general_row(const RowsArgs& A, BucketRecs R, bo
                 get(i, a, n1, n2, nullptr, false);
                 const int rel = c == v ? 0 : (n1 == c ? 1 : (n2 == c ? 2 : -1));
                 if (rel < 0) continue;
-                double rv[7];
+                double rv[KindTraits<KIND>::RVALS];
                 get(i, a, n1, n2, rv, true);
                 for (int t = 0; t < NV; ++t) sum[t] = FADD(sum[t], entry_from<KIND>(A, rv, a, s, rel, t));
             }
@@ -879,14 +885,15 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     extern __shared__ __align__(16) unsigned char smem_raw[];
     BucketRecs R;
     R.vals = reinterpret_cast<double*>(smem_raw);
-    R.n1 = reinterpret_cast<int*>(R.vals + RVALS * CAPB);
-    R.n2 = R.n1 + CAPB;
-    R.ka = reinterpret_cast<unsigned*>(R.n2 + CAPB);
+    constexpr int CAP = TR::CAP;
+    R.n1 = reinterpret_cast<int*>(R.vals + RVALS * CAP);
+    R.n2 = R.n1 + CAP;
+    R.ka = reinterpret_cast<unsigned*>(R.n2 + CAP);
     // compact staging of the bucket's CSR segment; reuses the records area once every row
     // holds its merged entries in registers
     double* st_val = reinterpret_cast<double*>(smem_raw);
     int32_t* st_col = reinterpret_cast<int32_t*>(st_val + TR::STAGE);
-    __shared__ unsigned char s_own[CAPB];
+    __shared__ unsigned char s_own[TR::CAP];
     __shared__ int s_vst[BV + 1];
     __shared__ double2 s_oq[BV];
     __shared__ double s_ow[BV];
@@ -912,13 +919,13 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         s_ow[i] = 0.0;  // (the weighted mass reads its W per triangle, k_tri_wt)
     }
     __syncthreads();
-    const bool overflow = s_vst[BV] > CAPB;
+    const bool overflow = s_vst[BV] > CAP;
     const int n = overflow ? 0 : s_vst[BV];
     for (int vl = tid; vl < nvb && !overflow; vl += NT)
         for (int j = s_vst[vl]; j < s_vst[vl + 1]; ++j) s_own[j] = (unsigned char)vl;
     // ---- s) the bucket's plan entries -> shared memory (coalesced)
     {  // all loads of a thread issued before the first store (one DRAM round trip)
-        constexpr int PER = (CAPB + NT - 1) / NT;
+        constexpr int PER = (CAP + NT - 1) / NT;
         unsigned lk[PER], l1[PER], l2[PER];
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
@@ -985,7 +992,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     // ---- a) per incidence (balanced over threads): gathers from the L2-resident arrays, the
     //         row of the element matrix -> shared memory
     {
-        constexpr int AU = FA_ROWS_AU;
+        constexpr int AU = KIND == FA_KIND_ELASTIC ? FA_ROWS_AU_E : FA_ROWS_AU;
         for (int i0 = tid; i0 < n; i0 += NT * AU) {
             unsigned ka[AU];
             Gathered g[AU];
@@ -1000,10 +1007,10 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
                 const int i = i0 + u * NT;
                 if (i >= n) break;
                 const int vl = s_own[i];
-                double rv[7];
+                double rv[RVALS];
                 incidence_values<KIND>(A, ka[u] >> 2, int(ka[u] & 3u), g[u], s_oq[vl], s_ow[vl], rv);
 #pragma unroll
-                for (int j = 0; j < RVALS; ++j) R.vals[j * CAPB + i] = rv[j];
+                for (int j = 0; j < RVALS; ++j) R.vals[j * CAP + i] = rv[j];
             }
         }
     }
