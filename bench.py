@@ -265,6 +265,15 @@ def run_reference(args):
 # ------------------------------------------------------------------------------------------
 # our arm
 # ------------------------------------------------------------------------------------------
+def _allreduce(dist, t, op, gloo):
+    if gloo:
+        c = t.cpu()
+        dist.all_reduce(c, op=op)
+        return c.to(t.device)
+    dist.all_reduce(t, op=op)
+    return t
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -278,10 +287,19 @@ def run_ours(args):
     rank, world, local = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    # functional check of the N > 1 path on a single-GPU box (never a measurement):
+    # FEMASM_BENCH_SAME_DEVICE=1 puts every rank on cuda:0, FEMASM_BENCH_BACKEND=gloo
+    same_dev = os.environ.get("FEMASM_BENCH_SAME_DEVICE") == "1"
+    gpu = 0 if same_dev else local
+    torch.cuda.set_device(gpu)
+    dev = torch.device("cuda", gpu)
+    gloo = world > 1 and os.environ.get("FEMASM_BENCH_BACKEND", "nccl") == "gloo"
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("FEMASM_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     kind, n, lam, mu, sm = mesh_for(args.config, args.seed)
     areas = fa.compute_areas(sm.vertices, sm.connectivity)
@@ -314,7 +332,11 @@ def run_ours(args):
             plan.build(me_d)  # current stream (the capture stream inside a graph capture)
         plan.assemble_into(kind, q_use, a_d, w_d, lam, mu, rowptr, col, val, res)
         if world > 1:
-            dist.all_gather_into_tensor(nnz_t, rowptr[-1:])  # row-offset allgather (NCCL)
+            if gloo:  # functional-check backend (CPU tensors)
+                parts = [torch.empty(1, dtype=torch.int64) for _ in range(world)]
+                dist.all_gather(parts, rowptr[-1:].cpu())
+            else:
+                dist.all_gather_into_tensor(nnz_t, rowptr[-1:])  # row-offset allgather (NCCL)
 
     # one cold (or warm) step captured as a CUDA graph: the launches of the ~8 kernels of a
     # step are replayed without host round trips (the kernel timer events are graph nodes)
@@ -365,7 +387,7 @@ def run_ours(args):
     for _ in range(args.warmup):
         step(True)
     torch.cuda.synchronize()
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(gpu)
     clocks.start()
     if world > 1:
         dist.barrier()
@@ -385,9 +407,9 @@ def run_ours(args):
     warm_ms = sum(warm_step) / len(warm_step)
     t = torch.tensor([total_ms, warm_ms, float(np.mean(rows_ms))], dtype=torch.float64, device=dev)
     if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        t = _allreduce(dist, t, dist.ReduceOp.MAX, gloo)
         nz = torch.tensor([local_nnz], dtype=torch.int64, device=dev)
-        dist.all_reduce(nz)
+        nz = _allreduce(dist, nz, dist.ReduceOp.SUM, gloo)
         total_nnz = int(nz.item())
     else:
         total_nnz = local_nnz
@@ -413,11 +435,11 @@ def run_ours(args):
             d2h = rp.numel() * 8 + nnz_e * (4 + 8)
         te = torch.tensor([max(ts), statistics.median(ts)], dtype=torch.float64, device=dev)
         if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+            te = _allreduce(dist, te, dist.ReduceOp.MAX, gloo)
         h2d = ha.bytes_h2d() * world
         d2h_t = torch.tensor([d2h], dtype=torch.int64, device=dev)
         if world > 1:
-            dist.all_reduce(d2h_t)
+            d2h_t = _allreduce(dist, d2h_t, dist.ReduceOp.SUM, gloo)
         e2e = {"value": sm.nme / float(te[1]), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h_t.item()), "timing": "wall clock per call (median), max over ranks",
                "api": "paper_1305_3122_b200.optv2.HostAssembler.run (C ABI fa_plan_build + fa_assemble)"}
