@@ -68,6 +68,7 @@ class HostAssembler:
         self._cap = None
         self.h_rowptr = torch.empty(self.rows + 1, dtype=torch.int64, pin_memory=True)
         self.h_nnz = torch.empty(1, dtype=torch.int64, pin_memory=True)
+        self._side = None
 
     def _ensure_capacity(self):
         torch = require_cuda()
@@ -90,13 +91,20 @@ class HostAssembler:
             s = src if isinstance(src, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(src))
             dst.copy_(s.view(dst.shape), non_blocking=True)
 
-        with torch.cuda.stream(st):
-            h2d(self.me, me)
+        # the connectivity first (the plan needs only it); the numeric inputs travel on a side
+        # stream while the plan is built
+        if self._side is None:
+            self._side = torch.cuda.Stream()
+        self._side.wait_stream(st)
+        with torch.cuda.stream(self._side):
             h2d(self.q, q)
             h2d(self.areas, areas)
             h2d(self.w, w)
+        with torch.cuda.stream(st):
+            h2d(self.me, me)
             self.plan.build(self.me, st)
             self._ensure_capacity()
+            st.wait_stream(self._side)
             self.plan.assemble_into(self.kind, self.q, self.areas, self.w, lam, mu, self.rowptr, self.col,
                                     self.val, self.res, st)
             self.h_rowptr.copy_(self.rowptr, non_blocking=True)
