@@ -265,3 +265,17 @@ def test_two_level_plan(monkeypatch, kind, coarse_log2):
         got, _ = plan_assemble(kind, sm.vertices, sm.connectivity, areas, sm.weights, 1.5, 0.6, v0=v0, v1=v1)
         sub = fo.assemble_row_block(kind, sm.vertices, sm.connectivity, areas, sm.weights, 1.5, 0.6, v0, v1)
         assert_same_csc(got, sub, f"{kind} block {v0}:{v1}")
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_vertex_above_bucket_capacity(kind):
+    """A hub of degree 1300 overflows its 128-vertex bucket's shared-memory slots (CAPB = 1024):
+    every row of that bucket takes the global-memory general path; the plan heap-sorts the
+    hub's incidences.  Bitwise against the oracle."""
+    V, C = fan_mesh(1300, n_rings=2)
+    areas = fo.triangle_areas(V, C)
+    w = 0.5 + (np.arange(V.shape[0]) % 5) * 0.3
+    ref = c_oracle.assemble(kind, V, C, areas, w, 1.3, 0.4)
+    got, r = plan_assemble(kind, V, C, areas, w, 1.3, 0.4)
+    assert r.heavy_rows > 0
+    assert_same_csc(got, ref, f"{kind} hub 1300")
