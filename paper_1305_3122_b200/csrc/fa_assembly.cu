@@ -145,6 +145,10 @@ struct PlanArgs {
     fa_result* res;
 };
 
+__device__ __forceinline__ bool tri_ids_valid(int c0, int c1, int c2, int64_t nq) {
+    return unsigned(c0) < nq && unsigned(c1) < nq && unsigned(c2) < nq;
+}
+
 // K1: owned incidences per (block, part) and per part; index validation (sparse.py:131-137 semantics: first bad
 // position in the flattened connectivity).
 __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_constant__ PlanArgs P) {
@@ -164,14 +168,14 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
         for (int u = 0; u < U; ++u) {
             const int64_t k = k0u + u * PLACE_THREADS;
             if (k >= k1) break;
+            // a triangle with an out-of-range corner is reported and left out entirely, so no
+            // incidence ever names an invalid neighbour
+            const bool ok = tri_ids_valid(c[u][0], c[u][1], c[u][2], P.nq);
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 const int64_t v = c[u][a];
-                if (v < 0 || v >= P.nq) {
-                    atomic_min_i64(&P.res->index_error_pos, 3 * k + a);
-                    continue;
-                }
-                if (v >= P.v0 && v < P.v1) atomicAdd(&s_cnt[(v - P.v0) >> P.plog], 1u);
+                if (v < 0 || v >= P.nq) atomic_min_i64(&P.res->index_error_pos, 3 * k + a);
+                if (ok && v >= P.v0 && v < P.v1) atomicAdd(&s_cnt[(v - P.v0) >> P.plog], 1u);
             }
         }
     }
@@ -260,12 +264,13 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
         for (int t = 0; t < TPT; ++t) {
             const int64_t k = r0 + t * PLACE_THREADS + tid;
             const int c[3] = {cur[t][0], cur[t][1], cur[t][2]};
+            const bool ok = tri_ids_valid(c[0], c[1], c[2], P.nq);  // as k_part_hist
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 const int64_t v = c[a];
                 const int j = 3 * t + a;
                 part[j] = 0xffffffffu;
-                if (v >= P.v0 && v < P.v1 && v < P.nq) {
+                if (ok && v >= P.v0 && v < P.v1) {
                     const unsigned vl = unsigned(v - P.v0);
                     part[j] = vl >> P.plog;
                     rank[j] = atomicAdd(&s_cnt[part[j]], 1u);
@@ -1346,7 +1351,7 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const unsigned long lon
 #define FA_TRI_WT_U 4
 #endif
 constexpr int TRI_WT_U = FA_TRI_WT_U;  // triangles in flight per thread
-__global__ void __launch_bounds__(256) k_tri_wt(const int32_t* __restrict__ me, int64_t nme,
+__global__ void __launch_bounds__(256) k_tri_wt(const int32_t* __restrict__ me, int64_t nme, int64_t nq,
                                                  const double* __restrict__ areas, const double* __restrict__ w,
                                                  double4* __restrict__ Wt) {
     const uint64_t pol = l2_evict_first_policy();
@@ -1368,7 +1373,8 @@ __global__ void __launch_bounds__(256) k_tri_wt(const int32_t* __restrict__ me, 
     for (int u = 0; u < TRI_WT_U; ++u)
         if (k0 + u * 256 < nme)
 #pragma unroll
-            for (int a = 0; a < 3; ++a) wc[u][a] = ld_keep_f64(w + c[u][a], keep);
+            for (int a = 0; a < 3; ++a)  // out-of-range ids (reported by the plan build) read nothing
+                wc[u][a] = unsigned(c[u][a]) < nq ? ld_keep_f64(w + c[u][a], keep) : 0.0;
 #pragma unroll
     for (int u = 0; u < TRI_WT_U; ++u) {
         const int64_t k = k0 + u * 256;
@@ -1664,8 +1670,8 @@ extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double
     if (kind == FA_KIND_MASSW) {  // the triangles' W once (k_tri_wt), gathered per incidence
         if (!d_areas) { set_error("WEIGHTED_MASS requires areas"); return FA_ERR_ARGUMENT; }
         if (!p->Wt) FA_CUDA(cudaMalloc(&p->Wt, sizeof(double4) * size_t(p->nme)));
-        k_tri_wt<<<unsigned((p->nme + 256 * TRI_WT_U - 1) / (256 * TRI_WT_U)), 256, 0, st>>>(p->me, p->nme, d_areas,
-                                                                                           d_w, p->Wt);
+        k_tri_wt<<<unsigned((p->nme + 256 * TRI_WT_U - 1) / (256 * TRI_WT_U)), 256, 0, st>>>(p->me, p->nme, p->nq,
+                                                                                           d_areas, d_w, p->Wt);
         FA_LAUNCH_CHECK("k_tri_wt");
         A.Wt = p->Wt;
     }

@@ -40,93 +40,162 @@ __all__ = [
 ]
 
 
+class _Slot:
+    """Device inputs/outputs and pinned host outputs of one in-flight step."""
+
+    def __init__(self, torch, dev, kind, nq, nme, rows, needs_q, recompute_areas):
+        self.me = torch.empty((nme, 3), dtype=torch.int32, device=dev)
+        self.q = torch.empty((nq, 2), dtype=torch.float64, device=dev) if needs_q else None
+        self.areas = None if recompute_areas else torch.empty(nme, dtype=torch.float64, device=dev)
+        self.w = torch.empty(nq, dtype=torch.float64, device=dev) if kind == "massw" else None
+        self.rowptr = torch.empty(rows + 1, dtype=torch.int64, device=dev)
+        self.res = ResultBlock()
+        self.h_rowptr = torch.empty(rows + 1, dtype=torch.int64, pin_memory=True)
+        self.bres = torch.empty(_lib.RESULT_WORDS, dtype=torch.int64, device=dev)  # the plan build's block
+        self.h_res = torch.empty(2 * _lib.RESULT_WORDS, dtype=torch.int64, pin_memory=True)
+        self.col = self.val = self.h_col = self.h_val = None
+        self.ev_me, self.ev_in, self.ev_comp, self.ev_meta, self.ev_out = (torch.cuda.Event() for _ in range(5))
+        self.ticket = None  # step occupying the slot, until its result is collected
+        self.used = False
+
+
 class HostAssembler:
     """Reusable end-to-end assembler for one (kind, nq, nme, row block).
 
     ``run(me, q, areas, w, lam, mu)`` takes host arrays (pinned torch CPU tensors for
     overlap-free DMA, or numpy), copies them to the device, builds the plan, assembles and
-    copies rowptr/col/val back into pinned host tensors.  Returns (rowptr, col, val) host
-    tensors (views of the pinned buffers, valid until the next run) and the fa_result.
+    copies rowptr/col/val back into pinned host tensors.  Returns (rowptr, col, val, nnz): host
+    tensors (views of the pinned buffers, valid until the slot is reused) and the entry count.
+
+    ``submit`` / ``result`` split a call in two so that a stream of problems of one size
+    pipelines over ``depth`` buffer slots: the host->device copy of step i+1 and its plan +
+    assembly run while the device->host copy of step i is in flight (PCIe is full duplex; the
+    copies use side streams, the kernels the caller's stream; the entry arrays of step i go on
+    a stream of their own so they never queue behind step i+1's kernels).  ``run`` = submit +
+    result.
+    The result blocks of the last collected step are ``last_result`` (assembly: nnz, first
+    degenerate triangle) and ``last_build_result`` (plan build: first out-of-range vertex id).
     """
 
     def __init__(self, kind: str, nq: int, nme: int, row_begin: int = 0, row_end: int | None = None,
-                 recompute_areas: bool = False):
+                 recompute_areas: bool = False, depth: int = 2):
         torch = require_cuda()
+        if depth < 1:
+            raise ValueError("depth must be >= 1")
         self.kind = kind
         self.nq, self.nme = int(nq), int(nme)
         self.recompute_areas = bool(recompute_areas)
         dev = device()
         self.plan = AssemblyPlan(nme, nq, row_begin, row_end)
-        self.me = torch.empty((self.nme, 3), dtype=torch.int32, device=dev)
-        needs_q = kind in ("stiff", "elastic") or recompute_areas
-        self.q = torch.empty((self.nq, 2), dtype=torch.float64, device=dev) if needs_q else None
-        self.areas = None if recompute_areas else torch.empty(self.nme, dtype=torch.float64, device=dev)
-        self.w = torch.empty(self.nq, dtype=torch.float64, device=dev) if kind == "massw" else None
         self.rows = self.plan.rows(kind)
-        self.rowptr = torch.empty(self.rows + 1, dtype=torch.int64, device=dev)
-        self.res = ResultBlock()
+        needs_q = kind in ("stiff", "elastic") or recompute_areas
+        self._slots = [_Slot(torch, dev, kind, self.nq, self.nme, self.rows, needs_q, self.recompute_areas)
+                       for _ in range(depth)]
+        self._h2d = torch.cuda.Stream()
+        self._meta = torch.cuda.Stream()  # row pointers + result blocks (waits for the kernels)
+        self._d2h = torch.cuda.Stream()   # entry arrays (issued by result(), never queued behind a later step)
+        self._next = 0
         self._cap = None
-        self.h_rowptr = torch.empty(self.rows + 1, dtype=torch.int64, pin_memory=True)
-        self.h_nnz = torch.empty(1, dtype=torch.int64, pin_memory=True)
-        self._side = None
+        self.last_result = self.last_build_result = None
 
-    def _ensure_capacity(self):
+    def _ensure_capacity(self, s: _Slot):
         torch = require_cuda()
         if self._cap is None:
-            cap = self.plan.capacity(self.kind)
+            self._cap = max(self.plan.capacity(self.kind), 1)
+        if s.col is None:
             dev = device()
-            self.col = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
-            self.val = torch.empty(max(cap, 1), dtype=torch.float64, device=dev)
-            self.h_col = torch.empty(max(cap, 1), dtype=torch.int32, pin_memory=True)
-            self.h_val = torch.empty(max(cap, 1), dtype=torch.float64, pin_memory=True)
-            self._cap = cap
+            s.col = torch.empty(self._cap, dtype=torch.int32, device=dev)
+            s.val = torch.empty(self._cap, dtype=torch.float64, device=dev)
+            s.h_col = torch.empty(self._cap, dtype=torch.int32, pin_memory=True)
+            s.h_val = torch.empty(self._cap, dtype=torch.float64, pin_memory=True)
 
-    def run(self, me, q=None, areas=None, w=None, lam=0.0, mu=0.0, stream=None):
+    def submit(self, me, q=None, areas=None, w=None, lam=0.0, mu=0.0, stream=None) -> int:
+        """Queue one step (asynchronous); returns its ticket for ``result``."""
         torch = require_cuda()
         st = stream or torch.cuda.current_stream()
+        ticket = self._next
+        s = self._slots[ticket % len(self._slots)]
+        if s.ticket is not None:  # the slot's previous step must be collected first
+            self.result(s.ticket)
+        self._next += 1
 
         def h2d(dst, src):
             if dst is None:
                 return
-            s = src if isinstance(src, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(src))
-            dst.copy_(s.view(dst.shape), non_blocking=True)
+            t = src if isinstance(src, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(src))
+            dst.copy_(t.view(dst.shape), non_blocking=True)
 
-        # the connectivity first (the plan needs only it); the numeric inputs travel on a side
-        # stream while the plan is built
-        if self._side is None:
-            self._side = torch.cuda.Stream()
-        self._side.wait_stream(st)
-        with torch.cuda.stream(self._side):
-            h2d(self.q, q)
-            h2d(self.areas, areas)
-            h2d(self.w, w)
+        # inputs: after the kernels that last read this slot; the connectivity first (the plan
+        # needs only it), the numeric inputs while the plan is built
+        if s.used:
+            self._h2d.wait_event(s.ev_comp)
+        else:
+            self._h2d.wait_stream(st)
+        with torch.cuda.stream(self._h2d):
+            h2d(s.me, me)
+            s.ev_me.record(self._h2d)
+            h2d(s.q, q)
+            h2d(s.areas, areas)
+            h2d(s.w, w)
+            s.ev_in.record(self._h2d)
         with torch.cuda.stream(st):
-            h2d(self.me, me)
-            self.plan.build(self.me, st)
-            self._ensure_capacity()
-            st.wait_stream(self._side)
-            self.plan.assemble_into(self.kind, self.q, self.areas, self.w, lam, mu, self.rowptr, self.col,
-                                    self.val, self.res, st)
-            self.h_rowptr.copy_(self.rowptr, non_blocking=True)
-            self.h_nnz.copy_(self.rowptr[-1:], non_blocking=True)
-        st.synchronize()
-        nnz = int(self.h_nnz[0])
-        with torch.cuda.stream(st):
-            self.h_col[:nnz].copy_(self.col[:nnz], non_blocking=True)
-            self.h_val[:nnz].copy_(self.val[:nnz], non_blocking=True)
-        st.synchronize()
-        return self.h_rowptr, self.h_col[:nnz], self.h_val[:nnz], nnz
+            st.wait_event(s.ev_me)
+            self.plan.build(s.me, st)
+            s.bres.copy_(self.plan._build_res.dev)  # stream-ordered: before the next build resets it
+            self._ensure_capacity(s)
+            st.wait_event(s.ev_in)
+            self.plan.assemble_into(self.kind, s.q, s.areas, s.w, lam, mu, s.rowptr, s.col, s.val, s.res, st)
+            s.ev_comp.record(st)
+        self._meta.wait_event(s.ev_comp)
+        with torch.cuda.stream(self._meta):  # sizes known on the host: row pointers + result blocks
+            s.h_res[: _lib.RESULT_WORDS].copy_(s.res.dev, non_blocking=True)
+            s.h_res[_lib.RESULT_WORDS:].copy_(s.bres, non_blocking=True)
+            s.h_rowptr.copy_(s.rowptr, non_blocking=True)
+            s.ev_meta.record(self._meta)
+        s.ticket = ticket
+        s.used = True
+        return ticket
+
+    def result(self, ticket: int):
+        """Wait for step ``ticket``; returns (rowptr, col, val, nnz) host views of its slot."""
+        torch = require_cuda()
+        s = self._slots[ticket % len(self._slots)]
+        if s.ticket != ticket:
+            raise ValueError(f"step {ticket} is not in flight (slot holds {s.ticket})")
+        s.ev_meta.synchronize()
+        r, rb = _lib.FaResult(), _lib.FaResult()
+        for i, (name, _) in enumerate(_lib.FaResult._fields_[:6]):
+            setattr(r, name, int(s.h_res[i]))
+            setattr(rb, name, int(s.h_res[_lib.RESULT_WORDS + i]))
+        self.last_result, self.last_build_result = r, rb
+        nnz = int(r.nnz)
+        if nnz > self._cap:  # the capacity is sized once, from the first step's plan
+            s.ticket = None
+            raise RuntimeError(f"assembly needs {nnz} entries, the buffers hold {self._cap}: the row block's "
+                               "incidence count grew; use a new HostAssembler for this connectivity")
+        self._d2h.wait_event(s.ev_comp)
+        with torch.cuda.stream(self._d2h):  # entry arrays: nnz is known now
+            s.h_col[:nnz].copy_(s.col[:nnz], non_blocking=True)
+            s.h_val[:nnz].copy_(s.val[:nnz], non_blocking=True)
+            s.ev_out.record(self._d2h)
+        s.ev_out.synchronize()
+        s.ticket = None
+        return s.h_rowptr, s.h_col[:nnz], s.h_val[:nnz], nnz
+
+    def run(self, me, q=None, areas=None, w=None, lam=0.0, mu=0.0, stream=None):
+        return self.result(self.submit(me, q, areas, w, lam, mu, stream))
 
     def bytes_h2d(self) -> int:
-        return sum(int(t.numel() * t.element_size()) for t in (self.me, self.q, self.areas, self.w) if t is not None)
+        s = self._slots[0]
+        return sum(int(t.numel() * t.element_size()) for t in (s.me, s.q, s.areas, s.w) if t is not None)
 
 
 def _host_assemble(kind, nq, nme, me, q=None, areas=None, w=None, lam=0.0, mu=0.0) -> CscMatrix:
     me = connectivity_int32(np.asarray(me).reshape(int(nme), 3))
-    a = HostAssembler(kind, nq, nme)
+    a = HostAssembler(kind, nq, nme, depth=1)
     rowptr, col, val, nnz = a.run(me, q, areas, w, lam, mu)
-    r = a.res.fetch()
-    if r.index_error_pos != _lib.INT64_MAX:
+    r = a.last_result
+    if a.last_build_result.index_error_pos != _lib.INT64_MAX:
         raise ValueError("connectivity index out of range [0, nq)")
     if r.degenerate_index != _lib.INT64_MAX:
         from .mesh import DegenerateTriangleError

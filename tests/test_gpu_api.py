@@ -196,3 +196,54 @@ def test_mesh_text_roundtrip_and_generators(golden, tmp_path):
         p = tmp_path / f"{name}.msh"
         fa.write_mesh(mesh, p)
         assert fa.read_mesh(p) == mesh
+
+
+@pytest.mark.parametrize("kind", ("massw", "stiff", "elastic"))
+def test_host_assembler_pipelined_slots(golden, kind):
+    """submit/result over two buffer slots: step i+1's copies and kernels are queued before
+    step i is collected; every step must equal its own reference assembly."""
+    import torch
+
+    names = ["seeded_n16_s0", "seeded_n16_s1"] * 3
+    V0, C0 = golden[f"{names[0]}/V"], golden[f"{names[0]}/C"]
+    ha = fa.HostAssembler(kind, V0.shape[0], C0.shape[0], depth=2)
+    pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()  # noqa: E731
+    inputs = [(pin(golden[f"{n}/C"].astype(np.int32)), pin(golden[f"{n}/V"]), pin(golden[f"{n}/areas"]),
+               pin(golden[f"{n}/w"]) if kind == "massw" else None) for n in names]
+    tickets, got = [], []
+    for i, (me, q, a, w) in enumerate(inputs):
+        lam, mu = golden[f"{names[i]}/{kind}/lam_mu"]
+        tickets.append(ha.submit(me, q if kind != "massw" else None, a, w, lam, mu))
+        if i >= 1:
+            rp, cc, vv, nnz = ha.result(tickets[i - 1])
+            got.append((rp.numpy().copy(), cc.numpy().astype(np.int64), vv.numpy().copy()))
+    rp, cc, vv, nnz = ha.result(tickets[-1])
+    got.append((rp.numpy().copy(), cc.numpy().astype(np.int64), vv.numpy().copy()))
+    for n, g in zip(names, got):
+        ref = tuple(golden[f"{n}/{kind}/{f}"] for f in ("col_ptr", "row_idx", "values"))
+        assert_same_csc(g, ref, n)
+    with pytest.raises(ValueError, match="not in flight"):
+        ha.result(tickets[-1])
+
+
+@pytest.mark.parametrize("kind", ("mass", "massw", "stiff", "elastic"))
+def test_paper_entry_point_rejects_out_of_range_ids(golden, kind):
+    """An out-of-range vertex id raises ValueError (csc_from_triplets, sparse.py:131-137); the
+    triangle is left out of the plan, so no kernel reads past q / w."""
+    name = "seeded_n16_s0"
+    V, C, w, areas = (golden[f"{name}/{f}"] for f in ("V", "C", "w", "areas"))
+    nq, nme = V.shape[0], C.shape[0]
+    bad = C.copy()
+    bad[7, 1] = nq + 1000
+    bad[9, 2] = -5
+    call = {
+        "mass": lambda c: fa.MassAssemblingP1OptV2(nq, nme, c, areas),
+        "massw": lambda c: fa.MassWAssemblingP1OptV2(nq, nme, c, areas, w),
+        "stiff": lambda c: fa.StiffAssemblingP1OptV2(nq, nme, V, c, areas),
+        "elastic": lambda c: fa.StiffElasAssemblingP1OptV2(nq, nme, V, c, areas, *golden[f"{name}/elastic/lam_mu"]),
+    }[kind]
+    with pytest.raises(ValueError, match="out of range"):
+        call(bad)
+    m = call(C)  # the device is still healthy
+    ref = tuple(golden[f"{name}/{kind}/{f}"] for f in ("col_ptr", "row_idx", "values"))
+    assert_same_csc((m.col_ptr, m.row_idx, m.values), ref, kind)
