@@ -83,7 +83,10 @@ constexpr int PLAN_THREADS = 1024;
 constexpr int SORT_THREADS = 512;   // k_part_sort (2 blocks / SM, 64 registers)
 constexpr int PLACE_THREADS = 1024;  // k_part_hist / k_part_place block size
 constexpr int PLACE_BLOCKS_PER_SM = 1;
-constexpr int PLACE_TRI = 2048;    // triangles per placement round
+#ifndef FA_PLACE_TRI
+#define FA_PLACE_TRI 2048
+#endif
+constexpr int PLACE_TRI = FA_PLACE_TRI;  // triangles per placement round
 constexpr int SPLIT_MIN = 8192;    // fine parts above which placement goes through coarse parts
 constexpr int SPLIT_COARSE = 1024; // coarse parts of a two-level plan (at most)
 constexpr int SORT_CAP = 7680;     // part incidences sorted in shared memory (2 blocks / SM)
