@@ -685,8 +685,8 @@ template <int KIND>
 __device__ __forceinline__ void incidence_values(const RowsArgs& A, unsigned k, int a, const Gathered& g,
                                                  double2 own_p, double own_w, double* out) {
     double ar = g.ar;
-    double2 c0, c1, c2;
-    if (KIND == FA_KIND_STIFF || KIND == FA_KIND_ELASTIC || !A.areas) {
+    double2 c0, c1, c2;  // corners in triangle order (area recomputation, elasticity)
+    if (KIND == FA_KIND_ELASTIC || !A.areas) {
         c0 = sel3(a, own_p, g.p2, g.p1);
         c1 = sel3(a, g.p1, own_p, g.p2);
         c2 = sel3(a, g.p2, g.p1, own_p);
@@ -699,29 +699,31 @@ __device__ __forceinline__ void incidence_values(const RowsArgs& A, unsigned k, 
         out[1] = m.o;
         out[2] = m.o;
     } else if constexpr (KIND == FA_KIND_MASSW) {
-        // W of the own corner a and of the corners a+1 (n1), a+2 (n2) (k_tri_wt)
-        const double Wo = sel3(a, g.wt.x, g.wt.y, g.wt.z), W1 = sel3(a, g.wt.y, g.wt.z, g.wt.x),
-                     W2 = sel3(a, g.wt.z, g.wt.x, g.wt.y);
-        // row a of assembly.py:236-241 in the triangle's corner order (additions are not
-        // associative, so each corner keeps its own formula):
-        //   a=0: diag (3*W0 + W1) + W2,  (0,1) (W0 + W1) + W2/2,  (0,2) (W0 + W1/2) + W2
-        //   a=1: diag (W0 + 3*W1) + W2,  (1,2) (W0/2 + W1) + W2,  (1,0) (W0 + W1) + W2/2
-        //   a=2: diag (W0 + W1) + 3*W2,  (2,0) (W0 + W1/2) + W2,  (2,1) (W0/2 + W1) + W2
-        const double W0t = sel3(a, Wo, W2, W1), W1t = sel3(a, W1, Wo, W2), W2t = sel3(a, W2, W1, Wo);
-        const double t0 = FMUL(3.0, Wo);
-        const double d01 = FADD(W0t, W1t);
-        out[0] = a == 0 ? FADD(FADD(t0, W1t), W2t) : (a == 1 ? FADD(FADD(W0t, t0), W2t) : FADD(d01, t0));
-        const double e10 = FADD(d01, FMUL(W2t, 0.5));                  // (0,1) == (1,0)
-        const double e20 = FADD(FADD(W0t, FMUL(W1t, 0.5)), W2t);       // (0,2) == (2,0)
-        const double e21 = FADD(FADD(FMUL(W0t, 0.5), W1t), W2t);       // (1,2) == (2,1)
-        out[1] = sel3(a, e10, e21, e20);
-        out[2] = sel3(a, e20, e10, e21);
+        // the six distinct entries of the triangle's matrix (assembly.py:236-241), with W in
+        // the triangle's corner order (k_tri_wt); row a picks three (additions are not
+        // associative, so every entry keeps the reference's own expression):
+        //   (0,0) (3*W0 + W1) + W2   (1,1) (W0 + 3*W1) + W2   (2,2) (W0 + W1) + 3*W2
+        //   (0,1) (W0 + W1) + W2/2   (0,2) (W0 + W1/2) + W2   (1,2) (W0/2 + W1) + W2
+        const double W0 = g.wt.x, W1 = g.wt.y, W2 = g.wt.z;
+        const double s01 = FADD(W0, W1);
+        const double d0 = FADD(FADD(FMUL(3.0, W0), W1), W2);
+        const double d1 = FADD(FADD(W0, FMUL(3.0, W1)), W2);
+        const double d2 = FADD(s01, FMUL(3.0, W2));
+        const double e01 = FADD(s01, FMUL(W2, 0.5));
+        const double e02 = FADD(FADD(W0, FMUL(W1, 0.5)), W2);
+        const double e12 = FADD(FADD(FMUL(W0, 0.5), W1), W2);
+        out[0] = sel3(a, d0, d1, d2);
+        out[1] = sel3(a, e01, e12, e02);  // (a, a+1)
+        out[2] = sel3(a, e02, e01, e12);  // (a, a+2)
     } else if constexpr (KIND == FA_KIND_STIFF) {
-        const int b1 = a == 2 ? 0 : a + 1, b2 = a == 0 ? 2 : a - 1;
-        const StiffTri m = stiff_prepare(c0, c1, c2, ar);
-        out[0] = stiff_entry(m, a, a);
-        out[1] = stiff_entry(m, a, b1);
-        out[2] = stiff_entry(m, a, b2);
+        // the edges opposite the own corner and the two neighbours are the reference's u, v, w
+        // (assembly.py:251-254) taken in local order - the same operand pairs, so the same bits
+        // - and row a is their dot products over 4*area (stiff_entry without the selects)
+        const double2 eo = dsub2(g.p1, g.p2), e1 = dsub2(g.p2, own_p), e2 = dsub2(own_p, g.p1);
+        const double a4 = FMUL(4.0, ar);
+        out[0] = FDIV(FADD(FADD(0.0, FMUL(eo.x, eo.x)), FMUL(eo.y, eo.y)), a4);
+        out[1] = FDIV(FADD(FADD(0.0, FMUL(eo.x, e1.x)), FMUL(eo.y, e1.y)), a4);
+        out[2] = FDIV(FADD(FADD(0.0, FMUL(eo.x, e2.x)), FMUL(eo.y, e2.y)), a4);
     } else {
         const ElasticTri m = elastic_prepare(c0, c1, c2, ar);
         const double P = FADD(A.lam, FMUL(2.0, A.mu));
@@ -975,8 +977,8 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     //    bucket's own look-back (after phase c) finds its predecessors' - nobody waits on the
     //    slow gathers of another bucket
     int64_t count = 0, excl = 0, total = 0;
+    unsigned sk[NC];
     if (EARLY && fast) {
-        unsigned sk[NC];
         row_keys(R, start, deg, sk);
         unsigned prev = 0xffffffffu, distinct = 0;
 #pragma unroll
@@ -1029,7 +1031,6 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     //         bincount of the reference); exact-zero sums stay as entries and are counted
     int64_t zeros = 0;
     double dsum[NV], run_val[NC + 1][NV];
-    unsigned sk[NC];
     int diag_at = -1;  // the diagonal is emitted right after run j == diag_at
 #pragma unroll
     for (int t = 0; t < NV; ++t) dsum[t] = 0.0;
@@ -1043,7 +1044,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
                     dsum[t] = FADD(dsum[t], record_entry<KIND>(A, R.vals, slot, int(R.ka[slot] & 3u), s, 0, t));
             }
         }
-        row_keys(R, start, deg, sk);
+        if (!EARLY) row_keys(R, start, deg, sk);  // scalar kinds: sorted once, kept from the count
         unsigned prev = 0xffffffffu;
         double sum[NV];
 #pragma unroll
