@@ -725,16 +725,35 @@ __device__ __forceinline__ void incidence_values(const RowsArgs& A, unsigned k, 
         out[1] = FDIV(FADD(FADD(0.0, FMUL(eo.x, e1.x)), FMUL(eo.y, e1.y)), a4);
         out[2] = FDIV(FADD(FADD(0.0, FMUL(eo.x, e2.x)), FMUL(eo.y, e2.y)), a4);
     } else {
-        const ElasticTri m = elastic_prepare(c0, c1, c2, ar);
-        const double P = FADD(A.lam, FMUL(2.0, A.mu));
+        // gradients of the own corner and the two neighbours from the edges opposite them (the
+        // reference's u, v, w in local order: same operands, same bits, assembly.py:195-211)
+        const double inv2a = FDIV(0.5, ar);
+        const double2 eo = dsub2(g.p1, g.p2), e1 = dsub2(g.p2, own_p), e2 = dsub2(own_p, g.p1);
+        const double2 gO = make_double2(FMUL(eo.y, inv2a), FMUL(-eo.x, inv2a));
+        const double L = A.lam, M = A.mu, P = FADD(A.lam, FMUL(2.0, A.mu));
+        // own 2x2 block (elastic_lower with A == B; (x, y) is the copy of (y, x))
+        out[0] = FMUL(FADD(FMUL(FMUL(P, gO.x), gO.x), FMUL(FMUL(M, gO.y), gO.y)), ar);
+        out[7] = FMUL(FADD(FMUL(FMUL(P, gO.y), gO.y), FMUL(FMUL(M, gO.x), gO.x)), ar);
+        out[6] = FMUL(FADD(FMUL(FMUL(L, gO.x), gO.y), FMUL(FMUL(M, gO.x), gO.y)), ar);
+        out[1] = out[6];
 #pragma unroll
-        for (int s = 0; s < 2; ++s)
-#pragma unroll
-            for (int rel = 0; rel < 3; ++rel) {
-                const int bl = rel == 0 ? a : (rel == 1 ? (a == 2 ? 0 : a + 1) : (a == 0 ? 2 : a - 1));
-#pragma unroll
-                for (int t = 0; t < 2; ++t) out[s * 6 + rel * 2 + t] = elastic_entry(m, 2 * a + s, 2 * bl + t, A.lam, A.mu, P);
-            }
+        for (int rel = 1; rel < 3; ++rel) {
+            const double2 e = rel == 1 ? e1 : e2;
+            const double2 gb = make_double2(FMUL(e.y, inv2a), FMUL(-e.x, inv2a));
+            // the lower-triangle entry puts the corner with the larger triangle index first
+            // (X) and takes the other's gradient first in every product (elastic_lower); the
+            // neighbour at corner a+1 is larger unless a == 2, the one at a+2 unless a == 0
+            const bool own_x = rel == 1 ? a == 2 : a != 0;
+            const double2 gX = own_x ? gO : gb, gY = own_x ? gb : gO;
+            const double d00 = FADD(FMUL(FMUL(P, gY.x), gX.x), FMUL(FMUL(M, gY.y), gX.y));
+            const double d11 = FADD(FMUL(FMUL(P, gY.y), gX.y), FMUL(FMUL(M, gY.x), gX.x));
+            const double l10 = FADD(FMUL(FMUL(L, gY.x), gX.y), FMUL(FMUL(M, gY.y), gX.x));  // X's y, Y's x
+            const double l01 = FADD(FMUL(FMUL(L, gY.y), gX.x), FMUL(FMUL(M, gY.x), gX.y));  // X's x, Y's y
+            out[rel * 2] = FMUL(d00, ar);                          // (own x, b x)
+            out[6 + rel * 2 + 1] = FMUL(d11, ar);                  // (own y, b y)
+            out[6 + rel * 2] = FMUL(own_x ? l10 : l01, ar);        // (own y, b x)
+            out[rel * 2 + 1] = FMUL(own_x ? l01 : l10, ar);        // (own x, b y)
+        }
     }
 }
 
