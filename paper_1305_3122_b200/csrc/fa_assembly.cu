@@ -88,7 +88,12 @@ constexpr int PLACE_BLOCKS_PER_SM = 1;
 #endif
 constexpr int PLACE_TRI = FA_PLACE_TRI;  // triangles per placement round
 constexpr int SPLIT_MIN = 8192;    // fine parts above which placement goes through coarse parts
-constexpr int SPLIT_COARSE = 1024; // coarse parts of a two-level plan (at most)
+// records above this size do not stay in L2 between placement and sort, so the placement's
+// runs must be long (coarse parts) and a parallel split regroups them by fine part
+constexpr int64_t SPLIT_BYTES = int64_t(160) << 20;
+constexpr int SPLIT_COARSE = 256;  // coarse parts of a two-level plan (at most)
+constexpr int FINE_HIST_MAX = 49152;  // fine parts counted in k_part_hist's shared memory
+constexpr int SPLIT2_LOCAL = 1024;    // fine parts a k_part_split2 round ranks in shared memory
 constexpr int SORT_CAP = 7680;     // part incidences sorted in shared memory (2 blocks / SM)
 
 // Resets the result block and zeroes the counters the following kernels accumulate into
@@ -136,11 +141,15 @@ struct PlanArgs {
     int64_t nme, nq, v0, v1;
     int plog;               // part = (v - v0) >> plog
     int nparts;
+    int plog_f, nparts_f;   // fine parts (== the above unless a two-level plan)
+    bool fine_hist;         // two-level: K1 counts fine parts, K2 derives the coarse offsets
+    unsigned* part_off_f;   // nparts_f + 1: fine counts (K1), offsets (K2)
+    unsigned* fine_fill;    // nparts_f: k_part_split2 cursors
     int64_t chunk;          // triangles per block of K1 / K3
     unsigned* part_off;     // nparts + 1: counts (K1), exclusive offsets (K2)
     unsigned* part_fill;    // nparts: placement cursors
     unsigned* M;            // [blocks][nparts]: owned incidences of each K1/K3 block per part
-    uint4* rec;             // owned incidences grouped by part {k, vp << 2 | a, n1, n2}
+    uint4* rec;             // owned incidences grouped by part {k, vl << 2 | a, n1, n2}, vl = v - v0
     unsigned* skey;         // sorted by (vertex, k): k << 2 | a
     unsigned* sn1;          // neighbour at corner a+1
     unsigned* sn2;          // neighbour at corner a+2
@@ -156,7 +165,9 @@ __device__ __forceinline__ bool tri_ids_valid(int c0, int c1, int c2, int64_t nq
 // position in the flattened connectivity).
 __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_constant__ PlanArgs P) {
     extern __shared__ unsigned s_cnt[];
-    for (int i = threadIdx.x; i < P.nparts; i += PLACE_THREADS) s_cnt[i] = 0;
+    // counted per fine part in a two-level plan (the coarse counts are their sums)
+    const int hlog = P.fine_hist ? P.plog_f : P.plog, hn = P.fine_hist ? P.nparts_f : P.nparts;
+    for (int i = threadIdx.x; i < hn; i += PLACE_THREADS) s_cnt[i] = 0;
     __syncthreads();
     const int64_t k0 = int64_t(blockIdx.x) * P.chunk, k1 = min(P.nme, k0 + P.chunk);
     constexpr int U = 4;  // triangles in flight per thread
@@ -178,41 +189,58 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
             for (int a = 0; a < 3; ++a) {
                 const int64_t v = c[u][a];
                 if (v < 0 || v >= P.nq) atomic_min_i64(&P.res->index_error_pos, 3 * k + a);
-                if (ok && v >= P.v0 && v < P.v1) atomicAdd(&s_cnt[(v - P.v0) >> P.plog], 1u);
+                if (ok && v >= P.v0 && v < P.v1) atomicAdd(&s_cnt[(v - P.v0) >> hlog], 1u);
             }
         }
     }
     __syncthreads();
     unsigned* row = P.M + int64_t(blockIdx.x) * P.nparts;
-    for (int i = threadIdx.x; i < P.nparts; i += PLACE_THREADS) {
-        row[i] = s_cnt[i];
-        if (s_cnt[i]) atomicAdd(&P.part_off[i], s_cnt[i]);
+    if (!P.fine_hist) {
+        for (int i = threadIdx.x; i < P.nparts; i += PLACE_THREADS) {
+            row[i] = s_cnt[i];
+            if (s_cnt[i]) atomicAdd(&P.part_off[i], s_cnt[i]);
+        }
+    } else {
+        for (int i = threadIdx.x; i < P.nparts_f; i += PLACE_THREADS)
+            if (s_cnt[i]) atomicAdd(&P.part_off_f[i], s_cnt[i]);
+        const int F = 1 << (P.plog - P.plog_f);
+        for (int pc = threadIdx.x; pc < P.nparts; pc += PLACE_THREADS) {
+            unsigned c = 0;
+            for (int f = pc * F; f < min((pc + 1) * F, P.nparts_f); ++f) c += s_cnt[f];
+            row[pc] = c;
+        }
     }
 }
 
-// K2: exclusive scan of the part counts (one block; nparts <= MAX_PARTS = 8 per thread).
+// K2: exclusive scan of the part counts (one block, any part count).  Two-level plans with
+// fine counts (K1 fine_hist): the fine offsets, the split cursors, and the coarse offsets and
+// placement cursors taken at the coarse boundaries.
 __global__ void __launch_bounds__(PLAN_THREADS) k_part_scan(const __grid_constant__ PlanArgs P) {
     __shared__ unsigned s_warp[PLAN_THREADS / 32];
     __shared__ unsigned s_total;
-    constexpr int PER = MAX_PARTS / PLAN_THREADS;
-    unsigned c[PER], run = 0;
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-        const int i = threadIdx.x * PER + j;
-        c[j] = i < P.nparts ? P.part_off[i] : 0u;
-        run += c[j];
-    }
+    unsigned* cnt = P.fine_hist ? P.part_off_f : P.part_off;
+    const int n = P.fine_hist ? P.nparts_f : P.nparts;
+    const int per = (n + PLAN_THREADS - 1) / PLAN_THREADS;
+    const int i0 = threadIdx.x * per, i1 = min(n, i0 + per);
+    unsigned run = 0;
+    for (int i = i0; i < i1; ++i) run += cnt[i];
     unsigned ex = block_exclusive_scan<PLAN_THREADS>(run, s_warp, &s_total);
-#pragma unroll
-    for (int j = 0; j < PER; ++j) {
-        const int i = threadIdx.x * PER + j;
-        if (i < P.nparts) {
-            P.part_off[i] = ex;
-            P.part_fill[i] = ex;
-        }
-        ex += c[j];
+    for (int i = i0; i < i1; ++i) {
+        const unsigned c = cnt[i];
+        cnt[i] = ex;
+        if (P.fine_hist) P.fine_fill[i] = ex;
+        else P.part_fill[i] = ex;
+        ex += c;
     }
-    if (threadIdx.x == 0) P.part_off[P.nparts] = s_total;
+    if (threadIdx.x == 0) cnt[n] = s_total;
+    if (!P.fine_hist) return;
+    __syncthreads();  // fine offsets visible to the block
+    const int F = 1 << (P.plog - P.plog_f);
+    for (int pc = threadIdx.x; pc <= P.nparts; pc += PLAN_THREADS) {
+        const unsigned o = pc < P.nparts ? cnt[pc * F] : s_total;
+        P.part_off[pc] = o;
+        if (pc < P.nparts) P.part_fill[pc] = o;
+    }
 }
 
 // K3: incidence records grouped by part.  Each block reserves its range in every part once
@@ -232,7 +260,6 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
     __shared__ unsigned s_total;
     const int tid = threadIdx.x;
     const int64_t kb0 = int64_t(blockIdx.x) * P.chunk, kb1 = min(P.nme, kb0 + P.chunk);
-    const int pmask = (1 << P.plog) - 1;
     {
         const unsigned* row = P.M + int64_t(blockIdx.x) * P.nparts;
         for (int i = tid; i < P.nparts; i += PLACE_THREADS) {
@@ -277,7 +304,7 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
                     const unsigned vl = unsigned(v - P.v0);
                     part[j] = vl >> P.plog;
                     rank[j] = atomicAdd(&s_cnt[part[j]], 1u);
-                    rec[j] = make_uint4(unsigned(k), ((vl & unsigned(pmask)) << 2) | unsigned(a),
+                    rec[j] = make_uint4(unsigned(k), (vl << 2) | unsigned(a),
                                         unsigned(sel3(a, c[1], c[2], c[0])), unsigned(sel3(a, c[2], c[0], c[1])));
                 }
             }
@@ -346,7 +373,6 @@ __global__ void __launch_bounds__(SPLIT_THREADS, 1)
     const int tid = threadIdx.x;
     const int64_t pc = blockIdx.x;
     const unsigned off = part_off_c[pc], n = part_off_c[pc + 1] - off;
-    const unsigned fmask = (1u << plog) - 1;
     for (int f = tid; f < F; f += SPLIT_THREADS) s_cnt[f] = 0;
     __syncthreads();
     {
@@ -360,7 +386,7 @@ __global__ void __launch_bounds__(SPLIT_THREADS, 1)
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u)
-                if (y[u] != 0xffffffffu) atomicAdd(&s_cnt[(y[u] >> 2) >> plog], 1u);
+                if (y[u] != 0xffffffffu) atomicAdd(&s_cnt[((y[u] >> 2) >> plog) - (unsigned(pc) << (plog_c - plog))], 1u);
         }
     }
     __syncthreads();
@@ -385,10 +411,8 @@ __global__ void __launch_bounds__(SPLIT_THREADS, 1)
             fp[u] = 0xffffffffu;
             if (i < n) {
                 r[u] = rec[off + i];
-                const unsigned vp = r[u].y >> 2;
-                fp[u] = vp >> plog;
+                fp[u] = ((r[u].y >> 2) >> plog) - (unsigned(pc) << (plog_c - plog));
                 rank[u] = atomicAdd(&s_cnt[fp[u]], 1u);
-                r[u].y = ((vp & fmask) << 2) | (r[u].y & 3u);
             }
         }
         __syncthreads();
@@ -422,6 +446,91 @@ __global__ void __launch_bounds__(SPLIT_THREADS, 1)
             s_cnt[f] = 0;
         }
         __syncthreads();
+    }
+}
+
+// K3b' (two-level plans with fine counts): the placement's records regrouped by fine part,
+// in parallel over rounds of 3 * PLACE_TRI consecutive records (any block, any coarse part):
+// ranked by fine part in shared memory (relative to the round's smallest fine part), one range
+// per fine part reserved from the global cursors (K2), staged and written as coalesced runs.
+// Records whose fine part lies beyond the local window (only when coarse parts are smaller
+// than a round) take a cursor each.
+__global__ void __launch_bounds__(SPLIT_THREADS, 1)
+    k_part_split2(const uint4* __restrict__ rec, const unsigned* __restrict__ total_ptr, int plog,
+                  unsigned* __restrict__ fine_fill, uint4* __restrict__ rec2) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    constexpr int RI = 3 * PLACE_TRI;
+    constexpr int PER = RI / SPLIT_THREADS;
+    uint4* s_stage = reinterpret_cast<uint4*>(smem_raw);                       // [RI]
+    unsigned* s_cnt = reinterpret_cast<unsigned*>(s_stage + RI);             // [SPLIT2_LOCAL]
+    unsigned* s_lst = s_cnt + SPLIT2_LOCAL;                                  // [SPLIT2_LOCAL]
+    unsigned* s_gb = s_lst + SPLIT2_LOCAL;                                   // [SPLIT2_LOCAL]
+    unsigned short* s_fp = reinterpret_cast<unsigned short*>(s_gb + SPLIT2_LOCAL);  // [RI]
+    __shared__ unsigned s_fbase, s_total;
+    __shared__ unsigned s_warp[SPLIT_THREADS / 32];
+    static_assert(SPLIT_THREADS == SPLIT2_LOCAL, "one local fine part per thread in the scan");
+    const int tid = threadIdx.x;
+    const unsigned total = *total_ptr;
+    const uint64_t pol = l2_evict_first_policy();
+    s_cnt[tid] = 0;
+    for (unsigned r0 = blockIdx.x * unsigned(RI); r0 < total; r0 += gridDim.x * unsigned(RI)) {
+        if (tid == 0) s_fbase = 0xffffffffu;
+        uint4 r[PER];
+        unsigned f[PER], rank[PER];
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const unsigned i = r0 + u * SPLIT_THREADS + tid;
+            f[u] = 0xffffffffu;
+            if (i < total) {
+                asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                             : "=r"(r[u].x), "=r"(r[u].y), "=r"(r[u].z), "=r"(r[u].w)
+                             : "l"(rec + i), "l"(pol));
+                f[u] = (r[u].y >> 2) >> plog;
+            }
+        }
+        unsigned fmin = 0xffffffffu;
+#pragma unroll
+        for (int u = 0; u < PER; ++u) fmin = min(fmin, f[u]);
+        fmin = __reduce_min_sync(0xffffffffu, fmin);
+        __syncthreads();  // s_fbase reset (and the previous round's reads) done
+        if ((tid & 31) == 0) atomicMin(&s_fbase, fmin);
+        __syncthreads();
+        const unsigned fb = s_fbase;
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            if (f[u] == 0xffffffffu) continue;
+            const unsigned l = f[u] - fb;
+            if (l < unsigned(SPLIT2_LOCAL)) {
+                rank[u] = atomicAdd(&s_cnt[l], 1u);
+            } else {  // outside the local window: a cursor of its own
+                rec2[atomicAdd(&fine_fill[f[u]], 1u)] = r[u];
+                f[u] = 0xffffffffu;
+            }
+        }
+        __syncthreads();
+        const unsigned c = s_cnt[tid];
+        const unsigned ex = block_exclusive_scan<SPLIT_THREADS>(c, s_warp, &s_total);
+        s_lst[tid] = ex;
+        if (c) s_gb[tid] = atomicAdd(&fine_fill[fb + tid], c);
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            if (f[u] == 0xffffffffu) continue;
+            const unsigned l = f[u] - fb;
+            const unsigned pos = s_lst[l] + rank[u];
+            s_stage[pos] = r[u];
+            s_fp[pos] = (unsigned short)l;
+        }
+        __syncthreads();
+        const unsigned staged = s_total;
+        for (unsigned i = tid; i < staged; i += SPLIT_THREADS) {
+            const unsigned l = s_fp[i];
+            const uint4 v = s_stage[i];
+            asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(rec2 + s_gb[l] + (i - s_lst[l])),
+                         "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+                         : "memory");
+        }
+        s_cnt[tid] = 0;  // (own counter; the next round's first barrier orders it)
     }
 }
 
@@ -495,7 +604,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_cons
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u)
-                if (y[u] != 0xffffffffu) atomicAdd(&s_cur[y[u] >> 2], 1u);
+                if (y[u] != 0xffffffffu) atomicAdd(&s_cur[(y[u] >> 2) & unsigned(PV - 1)], 1u);
         }
     }
     __syncthreads();
@@ -530,7 +639,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_cons
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             if (i0 + u * SORT_THREADS < n) {
-                const unsigned pos = atomicAdd(&s_cur[r[u].y >> 2], 1u);
+                const unsigned pos = atomicAdd(&s_cur[(r[u].y >> 2) & unsigned(PV - 1)], 1u);
                 key[pos] = (r[u].x << 2) | (r[u].y & 3u);
                 n1[pos] = r[u].z;
                 n2[pos] = r[u].w;
@@ -1454,6 +1563,8 @@ struct fa_plan {
     unsigned* part_off;       // nparts + 1 (fine)
     unsigned* part_off_c;     // nparts_c + 1 (== part_off unless two_level)
     unsigned* part_fill;      // nparts_c
+    bool fine_hist;           // two_level with the fine counts from k_part_hist (parallel k_part_split2)
+    unsigned* fine_fill;      // nparts (fine_hist): split cursors
     unsigned* M;              // [nblk_place][nparts_c]
     uint4* rec;               // 3 * nme (owned incidences, grouped by placement part)
     uint4* rec2;              // two_level: regrouped by fine part
@@ -1476,7 +1587,7 @@ struct fa_plan {
 using namespace fa;
 
 static void plan_free(fa_plan* p) {
-    cudaFree(p->part_off); cudaFree(p->part_fill); cudaFree(p->M); cudaFree(p->rec); cudaFree(p->skey); cudaFree(p->sn1);
+    cudaFree(p->part_off); cudaFree(p->part_fill); cudaFree(p->fine_fill); cudaFree(p->M); cudaFree(p->rec); cudaFree(p->skey); cudaFree(p->sn1);
     cudaFree(p->sn2); cudaFree(p->ivptr); cudaFree(p->status);
     cudaFree(p->bsym); cudaFree(p->blen); cudaFree(p->bdrop); cudaFree(p->bshift); cudaFree(p->read_done);
     if (p->part_off_c != p->part_off) cudaFree(p->part_off_c);
@@ -1524,7 +1635,10 @@ extern "C" int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t ro
     // placement coalesces runs of ~3 * PLACE_TRI / parts records: above SPLIT_MIN fine parts it
     // works on coarse parts (<= SPLIT_COARSE of them) that k_part_split regroups
     p->plog_c = p->plog;
-    p->two_level = p->nparts > SPLIT_MIN;
+    // two levels when the fine parts are too many for the placement's shared memory, or when
+    // the records (16 bytes per owned incidence) do not stay in L2 until the sort reads them
+    const int64_t rec_bytes_est = int64_t(48) * nme / (nq > 0 ? nq : 1) * nv;
+    p->two_level = p->nparts > SPLIT_MIN || (rec_bytes_est > SPLIT_BYTES && p->nparts > SPLIT_COARSE);
     if (p->two_level)
         while (((nv + (int64_t(1) << p->plog_c) - 1) >> p->plog_c) > SPLIT_COARSE) ++p->plog_c;
     if (const char* env = getenv("FEMASM_B200_COARSE_LOG2")) {  // test hook: force a two-level plan
@@ -1536,6 +1650,9 @@ extern "C" int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t ro
     }
     p->nparts_c = int((nv + (int64_t(1) << p->plog_c) - 1) >> p->plog_c);
     if (p->nparts_c < 1) p->nparts_c = 1;
+    p->fine_hist = p->two_level && p->nparts <= FINE_HIST_MAX;
+    if (const char* env = getenv("FEMASM_B200_SPLIT1"))  // test hook: the one-block-per-coarse-part split
+        if (atoi(env) == 1) p->fine_hist = false;
     p->chunk_place = (nme + PLACE_BLOCKS_PER_SM * NUM_SMS_B200 - 1) / (PLACE_BLOCKS_PER_SM * NUM_SMS_B200);
     p->nblk_place = int((nme + p->chunk_place - 1) / p->chunk_place);
     p->ninc = -1;
@@ -1546,6 +1663,7 @@ extern "C" int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t ro
     if (e == cudaSuccess && p->two_level) e = cudaMalloc(&p->part_off_c, sizeof(unsigned) * (p->nparts_c + 1));
     if (e == cudaSuccess && p->two_level) e = cudaMalloc(&p->rec2, sizeof(uint4) * ninc_max);
     if (e == cudaSuccess) e = cudaMalloc(&p->part_fill, sizeof(unsigned) * p->nparts_c);
+    if (e == cudaSuccess && p->fine_hist) e = cudaMalloc(&p->fine_fill, sizeof(unsigned) * p->nparts);
     if (e == cudaSuccess) e = cudaMalloc(&p->M, sizeof(unsigned) * size_t(p->nblk_place) * p->nparts_c);
     if (e == cudaSuccess) e = cudaMalloc(&p->rec, sizeof(uint4) * ninc_max);
     if (e == cudaSuccess) e = cudaMalloc(&p->skey, sizeof(unsigned) * ninc_max);
@@ -1587,14 +1705,18 @@ extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, 
         return FA_OK;
     }
     p->me = d_me;
-    k_reset<<<4, 256, 0, st>>>(d_res, p->part_off_c, p->nparts_c + 1, nullptr, 0);  // result + part counts
+    // result + the part counts K1 accumulates (fine ones when it counts fine parts)
+    if (p->fine_hist) k_reset<<<8, 256, 0, st>>>(d_res, p->part_off, p->nparts + 1, nullptr, 0);
+    else k_reset<<<4, 256, 0, st>>>(d_res, p->part_off_c, p->nparts_c + 1, nullptr, 0);
     FA_LAUNCH_CHECK("k_reset");
     PlanArgs P;  // placement level (coarse parts when two_level)
     P.me = d_me; P.nme = p->nme; P.nq = p->nq; P.v0 = p->v0; P.v1 = p->v1;
     P.plog = p->plog_c; P.nparts = p->nparts_c; P.chunk = p->chunk_place;
     P.part_off = p->part_off_c; P.part_fill = p->part_fill; P.M = p->M; P.rec = p->rec;
     P.skey = p->skey; P.sn1 = p->sn1; P.sn2 = p->sn2; P.ivptr = p->ivptr; P.res = d_res;
-    const size_t hist_smem = sizeof(unsigned) * p->nparts_c;
+    P.plog_f = p->plog; P.nparts_f = p->nparts; P.fine_hist = p->fine_hist;
+    P.part_off_f = p->part_off; P.fine_fill = p->fine_fill;
+    const size_t hist_smem = sizeof(unsigned) * (p->fine_hist ? p->nparts : p->nparts_c);
     FA_CUDA(cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_smem)));
     k_part_hist<<<p->nblk_place, PLACE_THREADS, hist_smem, st>>>(P);
     FA_LAUNCH_CHECK("k_part_hist");
@@ -1604,7 +1726,19 @@ extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, 
     FA_CUDA(cudaFuncSetAttribute(k_part_place, cudaFuncAttributeMaxDynamicSharedMemorySize, int(place_smem)));
     k_part_place<<<p->nblk_place, PLACE_THREADS, place_smem, st>>>(P);
     FA_LAUNCH_CHECK("k_part_place");
-    if (p->two_level) {
+    if (p->fine_hist) {
+        constexpr int RI = 3 * PLACE_TRI;
+        const size_t split_smem = size_t(RI) * (sizeof(uint4) + sizeof(unsigned short)) + sizeof(unsigned) * 3 * SPLIT2_LOCAL;
+        FA_CUDA(cudaFuncSetAttribute(k_part_split2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(split_smem)));
+        int nsm = 0, dev = 0;
+        FA_CUDA(cudaGetDevice(&dev));
+        FA_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
+        const int64_t rounds = (3 * p->nme + RI - 1) / RI;  // upper bound on the owned incidences
+        const unsigned grid = unsigned(rounds < nsm ? rounds : nsm);
+        k_part_split2<<<grid, SPLIT_THREADS, split_smem, st>>>(p->rec, p->part_off + p->nparts, p->plog, p->fine_fill,
+                                                               p->rec2);
+        FA_LAUNCH_CHECK("k_part_split2");
+    } else if (p->two_level) {
         const int F = 1 << (p->plog_c - p->plog);
         const size_t split_smem = size_t(3 * PLACE_TRI) * (sizeof(uint4) + 1) + sizeof(unsigned) * 3 * F;
         FA_CUDA(cudaFuncSetAttribute(k_part_split, cudaFuncAttributeMaxDynamicSharedMemorySize, int(split_smem)));

@@ -249,12 +249,15 @@ def test_isolated_vertices_have_empty_rows():
         assert_same_csc(got, ref, kind)
 
 
+@pytest.mark.parametrize("split1", (0, 1))
 @pytest.mark.parametrize("coarse_log2", (11, 14))
 @pytest.mark.parametrize("kind", KINDS)
-def test_two_level_plan(monkeypatch, kind, coarse_log2):
-    """Row blocks above 8192 fine parts place incidences by coarse part and regroup them
-    (k_part_split); forced here on a small mesh and checked bitwise."""
+def test_two_level_plan(monkeypatch, kind, coarse_log2, split1):
+    """Large row blocks place incidences by coarse part and regroup them by fine part
+    (k_part_split2, or with split1 the one-block-per-coarse-part k_part_split); forced here
+    on a small mesh and checked bitwise."""
     monkeypatch.setenv("FEMASM_B200_COARSE_LOG2", str(coarse_log2))
+    monkeypatch.setenv("FEMASM_B200_SPLIT1", str(split1))
     sm = seeded_square_mesh(70, 4)  # 5041 vertices: 5 fine parts
     areas = fo.triangle_areas(sm.vertices, sm.connectivity)
     ref = c_oracle.assemble(kind, sm.vertices, sm.connectivity, areas, sm.weights, 1.5, 0.6)
@@ -265,6 +268,23 @@ def test_two_level_plan(monkeypatch, kind, coarse_log2):
         got, _ = plan_assemble(kind, sm.vertices, sm.connectivity, areas, sm.weights, 1.5, 0.6, v0=v0, v1=v1)
         sub = fo.assemble_row_block(kind, sm.vertices, sm.connectivity, areas, sm.weights, 1.5, 0.6, v0, v1)
         assert_same_csc(got, sub, f"{kind} block {v0}:{v1}")
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_two_level_sparse_parts(monkeypatch, kind):
+    """Vertex ids spread 2048 apart (3.4M mostly isolated vertices): a split round's records
+    span more fine parts than its shared-memory window, so some take a cursor each."""
+    monkeypatch.setenv("FEMASM_B200_COARSE_LOG2", "14")
+    sm = seeded_square_mesh(40, 3)
+    spread = 2048
+    V = np.zeros((sm.nq * spread, 2))
+    V[::spread] = sm.vertices
+    C = np.asarray(sm.connectivity, dtype=np.int64) * spread
+    areas = fo.triangle_areas(V, C)
+    w = 0.5 + np.arange(V.shape[0]) % 7 * 0.25
+    ref = c_oracle.assemble(kind, V, C, areas, w, 1.5, 0.6)
+    got, _ = plan_assemble(kind, V, C, areas, w, 1.5, 0.6)
+    assert_same_csc(got, ref, f"{kind} spread ids")
 
 
 @pytest.mark.parametrize("kind", KINDS)
