@@ -38,7 +38,7 @@ import numpy as np  # noqa: E402
 
 METRIC = "triangles assembled/sec (device-timed, incl. CSR build)"
 UNIT = "triangles/s"
-# our kernels launched per cold step (fa_plan_build + fa_assemble); memsets are not counted
+# our kernels launched per cold step (fa_assemble_cold = fa_plan_build + fa_assemble); memsets are not counted
 LAUNCHES_PER_STEP = ["k_reset", "k_part_hist", "k_part_scan", "k_part_place", "k_part_sort",
                      "k_reset", "k_tri_wt (weighted mass)", "k_rows", "k_compact (exits at once unless a sum was exactly zero)"]
 DEFAULT_CONFIG = "C2"
@@ -328,9 +328,11 @@ def run_ours(args):
     lib = _lib.lib()
 
     def step(cold=True):
-        if cold:
-            plan.build(me_d)  # current stream (the capture stream inside a graph capture)
-        plan.assemble_into(kind, q_use, a_d, w_d, lam, mu, rowptr, col, val, res)
+        # current stream (the capture stream inside a graph capture)
+        if cold:  # fa_assemble_cold: plan build + numeric pass (weighted mass: W records alongside the build)
+            plan.assemble_cold_into(me_d, kind, q_use, a_d, w_d, lam, mu, rowptr, col, val, res)
+        else:
+            plan.assemble_into(kind, q_use, a_d, w_d, lam, mu, rowptr, col, val, res)
         if world > 1:
             if gloo:  # functional-check backend (CPU tensors)
                 parts = [torch.empty(1, dtype=torch.int64) for _ in range(world)]

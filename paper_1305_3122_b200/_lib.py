@@ -39,6 +39,7 @@ EXPORTED_SYMBOLS = (
     "fa_plan_rows",
     "fa_plan_destroy",
     "fa_assemble",
+    "fa_assemble_cold",
     "fa_element_kg",
     "fa_build_ig_jg",
     "fa_batch_gradients",
@@ -82,6 +83,7 @@ _SIGNATURES = {
     "fa_plan_rows": (_I64, [_P, _I]),
     "fa_plan_destroy": (_I, [_P]),
     "fa_assemble": (_I, [_P, _I, _P, _P, _P, _D, _D, _P, _P, _P, _I64, _P, _P]),
+    "fa_assemble_cold": (_I, [_P, _P, _I, _P, _P, _P, _D, _D, _P, _P, _P, _I64, _P, _P, _P]),
     "fa_element_kg": (_I, [_I, _P, _I64, _P, _P, _P, _D, _D, _P, _P, _P]),
     "fa_build_ig_jg": (_I, [_I, _P, _I64, _P, _P, _P]),
     "fa_batch_gradients": (_I, [_P, _I64, _P, _P, _P, _P, _P]),

@@ -1582,11 +1582,21 @@ struct fa_plan {
     unsigned* read_done;      // nb (k_compact)
     int64_t ninc;             // -1 until read back
     bool built;
+    // fa_assemble_cold: W records computed on a low-priority side stream during the plan build
+    cudaStream_t s_hi, s_lo;  // created on first use
+    cudaEvent_t ev_fork, ev_wt, ev_done;
+    const void* wt_key[3];    // (me, areas, w) the prepared W records belong to; consumed once
+    bool wt_ready;
 };
 
 using namespace fa;
 
 static void plan_free(fa_plan* p) {
+    if (p->s_hi) cudaStreamDestroy(p->s_hi);
+    if (p->s_lo) cudaStreamDestroy(p->s_lo);
+    if (p->ev_fork) cudaEventDestroy(p->ev_fork);
+    if (p->ev_wt) cudaEventDestroy(p->ev_wt);
+    if (p->ev_done) cudaEventDestroy(p->ev_done);
     cudaFree(p->part_off); cudaFree(p->part_fill); cudaFree(p->fine_fill); cudaFree(p->M); cudaFree(p->rec); cudaFree(p->skey); cudaFree(p->sn1);
     cudaFree(p->sn2); cudaFree(p->ivptr); cudaFree(p->status);
     cudaFree(p->bsym); cudaFree(p->blen); cudaFree(p->bdrop); cudaFree(p->bshift); cudaFree(p->read_done);
@@ -1792,6 +1802,15 @@ extern "C" int fa_plan_capacity(fa_plan* p, int kind, int64_t* capacity) {
     return FA_OK;
 }
 
+// Weighted mass: the per-triangle W records of the plan's connectivity (k_tri_wt).
+static int launch_tri_wt(fa_plan* p, const double* d_areas, const double* d_w, cudaStream_t st) {
+    if (!p->Wt) FA_CUDA(cudaMalloc(&p->Wt, sizeof(double4) * size_t(p->nme)));
+    k_tri_wt<<<unsigned((p->nme + 256 * TRI_WT_U - 1) / (256 * TRI_WT_U)), 256, 0, st>>>(p->me, p->nme, p->nq, d_areas,
+                                                                                       d_w, p->Wt);
+    FA_LAUNCH_CHECK("k_tri_wt");
+    return FA_OK;
+}
+
 extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double* d_areas, const double* d_w,
                            double lam, double mu, int64_t* d_rowptr, int32_t* d_col, double* d_val, int64_t capacity,
                            fa_result* d_res, void* stream) {
@@ -1826,10 +1845,12 @@ extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double
     A.Wt = nullptr;
     if (kind == FA_KIND_MASSW) {  // the triangles' W once (k_tri_wt), gathered per incidence
         if (!d_areas) { set_error("WEIGHTED_MASS requires areas"); return FA_ERR_ARGUMENT; }
-        if (!p->Wt) FA_CUDA(cudaMalloc(&p->Wt, sizeof(double4) * size_t(p->nme)));
-        k_tri_wt<<<unsigned((p->nme + 256 * TRI_WT_U - 1) / (256 * TRI_WT_U)), 256, 0, st>>>(p->me, p->nme, p->nq,
-                                                                                           d_areas, d_w, p->Wt);
-        FA_LAUNCH_CHECK("k_tri_wt");
+        const bool prepared = p->wt_ready && p->wt_key[0] == p->me && p->wt_key[1] == d_areas && p->wt_key[2] == d_w;
+        p->wt_ready = false;
+        if (!prepared) {
+            const int rc = launch_tri_wt(p, d_areas, d_w, st);
+            if (rc != FA_OK) return rc;
+        }
         A.Wt = p->Wt;
     }
     int rc;
@@ -1850,5 +1871,48 @@ extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double
                                                      rpb, nrows, d_rowptr, d_col, d_val, d_res,
                                                      reinterpret_cast<unsigned*>(p->status + p->nb + 2));
     FA_LAUNCH_CHECK("k_compact");
+    return FA_OK;
+}
+
+// Plan build + numeric assembly in one call (the cold OptV2 of the reference API).  The plan
+// kernels and the row kernel run on a high-priority internal stream; for the weighted mass the
+// W records (which need no plan) are computed on a low-priority one at the same time, filling
+// the SM resources the plan kernels leave idle.  Both join back into `stream`.
+extern "C" int fa_assemble_cold(fa_plan* p, const int32_t* d_me, int kind, const double* d_q, const double* d_areas,
+                                const double* d_w, double lam, double mu, int64_t* d_rowptr, int32_t* d_col,
+                                double* d_val, int64_t capacity, fa_result* d_build_result, fa_result* d_result,
+                                void* stream) {
+    if (!p || !d_me || !d_build_result) { set_error("fa_assemble_cold: NULL argument"); return FA_ERR_ARGUMENT; }
+    cudaStream_t st = as_stream(stream);
+    const bool side = kind == FA_KIND_MASSW && d_areas && d_w && p->nb > 0;
+    if (!side) {
+        int rc = fa_plan_build(p, d_me, d_build_result, stream);
+        if (rc != FA_OK) return rc;
+        return fa_assemble(p, kind, d_q, d_areas, d_w, lam, mu, d_rowptr, d_col, d_val, capacity, d_result, stream);
+    }
+    if (!p->s_hi) {
+        int lo = 0, hi = 0;
+        FA_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        FA_CUDA(cudaStreamCreateWithPriority(&p->s_hi, cudaStreamNonBlocking, hi));
+        FA_CUDA(cudaStreamCreateWithPriority(&p->s_lo, cudaStreamNonBlocking, lo));
+        FA_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
+        FA_CUDA(cudaEventCreateWithFlags(&p->ev_wt, cudaEventDisableTiming));
+        FA_CUDA(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
+    }
+    FA_CUDA(cudaEventRecord(p->ev_fork, st));
+    FA_CUDA(cudaStreamWaitEvent(p->s_hi, p->ev_fork, 0));
+    FA_CUDA(cudaStreamWaitEvent(p->s_lo, p->ev_fork, 0));
+    int rc = fa_plan_build(p, d_me, d_build_result, p->s_hi);
+    if (rc != FA_OK) return rc;
+    rc = launch_tri_wt(p, d_areas, d_w, p->s_lo);
+    if (rc != FA_OK) return rc;
+    FA_CUDA(cudaEventRecord(p->ev_wt, p->s_lo));
+    FA_CUDA(cudaStreamWaitEvent(p->s_hi, p->ev_wt, 0));
+    p->wt_key[0] = d_me; p->wt_key[1] = d_areas; p->wt_key[2] = d_w;
+    p->wt_ready = true;
+    rc = fa_assemble(p, kind, d_q, d_areas, d_w, lam, mu, d_rowptr, d_col, d_val, capacity, d_result, p->s_hi);
+    if (rc != FA_OK) return rc;
+    FA_CUDA(cudaEventRecord(p->ev_done, p->s_hi));
+    FA_CUDA(cudaStreamWaitEvent(st, p->ev_done, 0));
     return FA_OK;
 }

@@ -68,6 +68,20 @@ class AssemblyPlan:
         )
         _lib.check(rc, "fa_assemble")
 
+    def assemble_cold_into(self, me_dev, kind, q, areas, w, lam, mu, rowptr, col, val, result: ResultBlock,
+                           stream=None) -> None:
+        """Plan build + numeric assembly in one asynchronous call (fa_assemble_cold): the cold
+        OptV2; the weighted mass's triangle records are computed concurrently with the build.
+        Build errors: check_build()."""
+        self._me = me_dev
+        self._capacity.clear()
+        rc = _lib.lib().fa_assemble_cold(
+            self._h, me_dev.data_ptr(), _lib.KIND_CODES[kind], _lib.ptr(q), _lib.ptr(areas), _lib.ptr(w),
+            float(lam), float(mu), rowptr.data_ptr(), col.data_ptr(), val.data_ptr(), int(col.numel()),
+            self._build_res.ptr, result.ptr, _lib.stream_handle(stream),
+        )
+        _lib.check(rc, "fa_assemble_cold")
+
     def assemble(self, kind, q=None, areas=None, w=None, lam=0.0, mu=0.0, stream=None):
         """Allocate outputs, assemble, synchronise; returns (rowptr, col, val, fa_result)."""
         torch = require_cuda()

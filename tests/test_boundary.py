@@ -62,6 +62,8 @@ def test_kernel_entry_points_validate_arguments():
     assert lib.fa_element_kg(7, None, 1, None, None, None, 0.0, 0.0, None, None, None) == _lib.FA_ERR_ARGUMENT
     assert "unknown matrix kind" in _lib.last_error()
     assert lib.fa_assemble(None, 0, None, None, None, 0.0, 0.0, None, None, None, 0, None, None) == _lib.FA_ERR_ARGUMENT
+    assert lib.fa_assemble_cold(None, None, 0, None, None, None, 0.0, 0.0, None, None, None, 0, None, None,
+                                None) == _lib.FA_ERR_ARGUMENT
     assert lib.fa_triplets_to_csc(None, None, None, 0, 0, 3, None, None, None, None, 0, None, None) == _lib.FA_ERR_ARGUMENT
     assert lib.fa_triplets_workspace(1000, 10, 10) > 1000 * 32
 

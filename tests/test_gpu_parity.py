@@ -299,3 +299,37 @@ def test_vertex_above_bucket_capacity(kind):
     got, r = plan_assemble(kind, V, C, areas, w, 1.3, 0.4)
     assert r.heavy_rows > 0
     assert_same_csc(got, ref, f"{kind} hub 1300")
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_assemble_cold_entry_point(kind):
+    """fa_assemble_cold (plan build + numeric pass in one call, the weighted mass's triangle
+    records on a side stream) equals the oracle bitwise, repeatedly and after a plain
+    fa_assemble on the same plan (the prepared records are consumed once)."""
+    import torch
+    from paper_1305_3122_b200.device import ResultBlock
+
+    sm = seeded_square_mesh(64, 5)
+    areas = fo.triangle_areas(sm.vertices, sm.connectivity)
+    ref = c_oracle.assemble(kind, sm.vertices, sm.connectivity, areas, sm.weights, 1.0, 0.5)
+    dev = torch.device("cuda")
+    me = torch.from_numpy(np.ascontiguousarray(sm.connectivity, dtype=np.int32)).to(dev)
+    q = torch.from_numpy(sm.vertices).to(dev)
+    a = torch.from_numpy(areas).to(dev)
+    w = torch.from_numpy(sm.weights).to(dev)
+    plan = fa.AssemblyPlan(sm.nme, sm.nq)
+    plan.build(me)
+    cap = plan.capacity(kind)
+    rowptr = torch.empty(plan.rows(kind) + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(cap, dtype=torch.int32, device=dev)
+    val = torch.empty(cap, dtype=torch.float64, device=dev)
+    for it in range(3):
+        res = ResultBlock()
+        if it == 1:
+            plan.assemble_into(kind, q, a, w, 1.0, 0.5, rowptr, col, val, res)
+        else:
+            plan.assemble_cold_into(me, kind, q, a, w, 1.0, 0.5, rowptr, col, val, res)
+        r = res.fetch()
+        plan.check_build()
+        got = (rowptr.cpu().numpy(), col[: r.nnz].cpu().numpy(), val[: r.nnz].cpu().numpy())
+        assert_same_csc(got, ref, f"{kind} cold call {it}")
