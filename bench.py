@@ -38,9 +38,11 @@ import numpy as np  # noqa: E402
 
 METRIC = "triangles assembled/sec (device-timed, incl. CSR build)"
 UNIT = "triangles/s"
-# our kernels launched per cold step (fa_assemble_cold = fa_plan_build + fa_assemble); memsets are not counted
-LAUNCHES_PER_STEP = ["k_reset", "k_part_hist", "k_part_scan", "k_part_place", "k_part_sort",
-                     "k_reset", "k_tri_wt (weighted mass)", "k_rows", "k_compact (exits at once unless a sum was exactly zero)"]
+def launches_per_step(kind):
+    """Our kernels launched per cold step (fa_assemble_cold); memsets are not counted."""
+    return (["k_reset", "k_part_hist", "k_part_scan", "k_part_place", "k_part_sort"]
+            + (["k_tri_wt (weighted-mass W records, side stream during the plan build)"] if kind == "massw" else [])
+            + ["k_reset", "k_rows", "k_compact (exits at once unless a sum was exactly zero)"])
 DEFAULT_CONFIG = "C2"
 DESCR = {
     "C1": "P1 mass, N=256 seeded jittered/permuted unit square",
@@ -492,8 +494,8 @@ def run_ours(args):
                      "what": "plan reused (vertex-sorted incidences cached): row kernel only"},
             "clocks": clock_info,
             "e2e": e2e,
-            "gpu_launches": len(LAUNCHES_PER_STEP) * args.steps,
-            "gpu_launches_detail": "per step: " + ", ".join(LAUNCHES_PER_STEP),
+            "gpu_launches": len(launches_per_step(kind)) * args.steps,
+            "gpu_launches_detail": "per step: " + ", ".join(launches_per_step(kind)),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
