@@ -17,8 +17,9 @@
 //     K3 part_place  per round of triangles: incidence records {k, vertex-in-part<<2|a, n1, n2}
 //                    ranked by part in shared memory, one range per (block, part) reserved once,
 //                    staged in part order and written as coalesced runs
-//     K3b part_split (two-level plans only: more than SPLIT_MIN parts) placement used coarse
-//                    parts; one block per coarse part regroups its records by fine part
+//     K3b part_split (two-level plans only: more than SPLIT_MIN parts, or records larger than
+//                    L2) placement used coarse parts; rounds of records (any block) are
+//                    regrouped by fine part, one range per (round, fine part)
 //     K4 part_sort   per part: counting sort by vertex in shared memory, each vertex's list
 //                    ordered by k; written as SoA (k<<2|a, n1, n2) + per-vertex offsets ivptr
 //   numeric
@@ -93,7 +94,7 @@ constexpr int SPLIT_MIN = 8192;    // fine parts above which placement goes thro
 constexpr int64_t SPLIT_BYTES = int64_t(160) << 20;
 constexpr int SPLIT_COARSE = 256;  // coarse parts of a two-level plan (at most)
 constexpr int FINE_HIST_MAX = 49152;  // fine parts counted in k_part_hist's shared memory
-constexpr int SPLIT2_LOCAL = 1024;    // fine parts a k_part_split2 round ranks in shared memory
+constexpr int SPLIT2_LOCAL = 1024;    // fine parts a k_part_split round ranks in shared memory
 constexpr int SORT_CAP = 7680;     // part incidences sorted in shared memory (2 blocks / SM)
 
 // Resets the result block and zeroes the counters the following kernels accumulate into
@@ -143,8 +144,9 @@ struct PlanArgs {
     int nparts;
     int plog_f, nparts_f;   // fine parts (== the above unless a two-level plan)
     bool fine_hist;         // two-level: K1 counts fine parts, K2 derives the coarse offsets
+    bool fine_global;       // fine parts beyond FINE_HIST_MAX: counted with global atomics
     unsigned* part_off_f;   // nparts_f + 1: fine counts (K1), offsets (K2)
-    unsigned* fine_fill;    // nparts_f: k_part_split2 cursors
+    unsigned* fine_fill;    // nparts_f: k_part_split cursors
     int64_t chunk;          // triangles per block of K1 / K3
     unsigned* part_off;     // nparts + 1: counts (K1), exclusive offsets (K2)
     unsigned* part_fill;    // nparts: placement cursors
@@ -165,8 +167,11 @@ __device__ __forceinline__ bool tri_ids_valid(int c0, int c1, int c2, int64_t nq
 // position in the flattened connectivity).
 __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_constant__ PlanArgs P) {
     extern __shared__ unsigned s_cnt[];
-    // counted per fine part in a two-level plan (the coarse counts are their sums)
-    const int hlog = P.fine_hist ? P.plog_f : P.plog, hn = P.fine_hist ? P.nparts_f : P.nparts;
+    // counted per fine part in a two-level plan (the coarse counts are their sums); beyond
+    // FINE_HIST_MAX fine parts the fine counts go to global memory and shared memory keeps
+    // the coarse ones
+    const bool fs = P.fine_hist && !P.fine_global;
+    const int hlog = fs ? P.plog_f : P.plog, hn = fs ? P.nparts_f : P.nparts;
     for (int i = threadIdx.x; i < hn; i += PLACE_THREADS) s_cnt[i] = 0;
     __syncthreads();
     const int64_t k0 = int64_t(blockIdx.x) * P.chunk, k1 = min(P.nme, k0 + P.chunk);
@@ -189,7 +194,10 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
             for (int a = 0; a < 3; ++a) {
                 const int64_t v = c[u][a];
                 if (v < 0 || v >= P.nq) atomic_min_i64(&P.res->index_error_pos, 3 * k + a);
-                if (ok && v >= P.v0 && v < P.v1) atomicAdd(&s_cnt[(v - P.v0) >> hlog], 1u);
+                if (ok && v >= P.v0 && v < P.v1) {
+                    atomicAdd(&s_cnt[(v - P.v0) >> hlog], 1u);
+                    if (P.fine_global) atomicAdd(&P.part_off_f[(v - P.v0) >> P.plog_f], 1u);
+                }
             }
         }
     }
@@ -200,6 +208,8 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
             row[i] = s_cnt[i];
             if (s_cnt[i]) atomicAdd(&P.part_off[i], s_cnt[i]);
         }
+    } else if (P.fine_global) {
+        for (int i = threadIdx.x; i < P.nparts; i += PLACE_THREADS) row[i] = s_cnt[i];
     } else {
         for (int i = threadIdx.x; i < P.nparts_f; i += PLACE_THREADS)
             if (s_cnt[i]) atomicAdd(&P.part_off_f[i], s_cnt[i]);
@@ -352,111 +362,16 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
     }
 }
 
-// K3b (two-level plans, row blocks above SPLIT_MIN fine parts): one block per coarse part, its
-// records regrouped by fine part (1024 vertices) into rec2 - counts in shared memory give the
-// fine part offsets (contiguous inside the coarse part's range), then rounds of records are
-// ranked, staged in fine-part order and written as coalesced runs.  The sort then works on
-// fine parts only, in shared memory.
 constexpr int SPLIT_THREADS = 1024;
-__global__ void __launch_bounds__(SPLIT_THREADS, 1)
-    k_part_split(const uint4* __restrict__ rec, const unsigned* __restrict__ part_off_c, int plog_c, int plog,
-                 unsigned* __restrict__ part_off_f, int64_t nparts_f, uint4* __restrict__ rec2) {
-    extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int RI = 3 * PLACE_TRI;
-    constexpr int PER = RI / SPLIT_THREADS;
-    const int F = 1 << (plog_c - plog);  // fine parts per coarse part (<= 256)
-    uint4* s_stage = reinterpret_cast<uint4*>(smem_raw);          // [RI]
-    unsigned* s_cnt = reinterpret_cast<unsigned*>(s_stage + RI);  // [F]
-    unsigned* s_lst = s_cnt + F;                                  // [F]
-    unsigned* s_cur = s_lst + F;                                  // [F] global cursors
-    unsigned char* s_fp = reinterpret_cast<unsigned char*>(s_cur + F);  // [RI]
-    const int tid = threadIdx.x;
-    const int64_t pc = blockIdx.x;
-    const unsigned off = part_off_c[pc], n = part_off_c[pc + 1] - off;
-    for (int f = tid; f < F; f += SPLIT_THREADS) s_cnt[f] = 0;
-    __syncthreads();
-    {
-        const unsigned* ry = reinterpret_cast<const unsigned*>(rec + off) + 1;
-        for (unsigned i0 = tid; i0 < n; i0 += 8 * SPLIT_THREADS) {
-            unsigned y[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const unsigned i = i0 + u * SPLIT_THREADS;
-                y[u] = i < n ? ry[4 * size_t(i)] : 0xffffffffu;
-            }
-#pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (y[u] != 0xffffffffu) atomicAdd(&s_cnt[((y[u] >> 2) >> plog) - (unsigned(pc) << (plog_c - plog))], 1u);
-        }
-    }
-    __syncthreads();
-    if (tid == 0) {
-        unsigned run = 0;
-        for (int f = 0; f < F; ++f) {
-            const int64_t gf = (pc << (plog_c - plog)) + f;
-            s_cur[f] = off + run;
-            if (gf < nparts_f) part_off_f[gf] = off + run;
-            run += s_cnt[f];
-            s_cnt[f] = 0;
-        }
-        if (pc == int64_t(gridDim.x) - 1) part_off_f[nparts_f] = off + n;
-    }
-    __syncthreads();
-    for (unsigned r0 = 0; r0 < n; r0 += RI) {
-        uint4 r[PER];
-        unsigned fp[PER], rank[PER];
-#pragma unroll
-        for (int u = 0; u < PER; ++u) {
-            const unsigned i = r0 + u * SPLIT_THREADS + tid;
-            fp[u] = 0xffffffffu;
-            if (i < n) {
-                r[u] = rec[off + i];
-                fp[u] = ((r[u].y >> 2) >> plog) - (unsigned(pc) << (plog_c - plog));
-                rank[u] = atomicAdd(&s_cnt[fp[u]], 1u);
-            }
-        }
-        __syncthreads();
-        if (tid < 32) {  // local starts: exclusive scan of the round counts over the F fine parts
-            unsigned base = 0;
-            for (int f0 = 0; f0 < F; f0 += 32) {
-                const unsigned c = f0 + tid < F ? s_cnt[f0 + tid] : 0u;
-                const unsigned inc = warp_inclusive_scan(c);
-                if (f0 + tid < F) s_lst[f0 + tid] = base + inc - c;
-                base += __shfl_sync(0xffffffffu, inc, 31);
-            }
-        }
-        __syncthreads();
-#pragma unroll
-        for (int u = 0; u < PER; ++u) {
-            if (fp[u] != 0xffffffffu) {
-                const unsigned pos = s_lst[fp[u]] + rank[u];
-                s_stage[pos] = r[u];
-                s_fp[pos] = (unsigned char)fp[u];
-            }
-        }
-        __syncthreads();
-        const unsigned total = min(unsigned(RI), n - r0);
-        for (unsigned i = tid; i < total; i += SPLIT_THREADS) {
-            const unsigned f = s_fp[i];
-            rec2[s_cur[f] + (i - s_lst[f])] = s_stage[i];
-        }
-        __syncthreads();
-        for (int f = tid; f < F; f += SPLIT_THREADS) {
-            s_cur[f] += s_cnt[f];
-            s_cnt[f] = 0;
-        }
-        __syncthreads();
-    }
-}
 
-// K3b' (two-level plans with fine counts): the placement's records regrouped by fine part,
+// K3b (two-level plans): the placement's records regrouped by fine part,
 // in parallel over rounds of 3 * PLACE_TRI consecutive records (any block, any coarse part):
 // ranked by fine part in shared memory (relative to the round's smallest fine part), one range
 // per fine part reserved from the global cursors (K2), staged and written as coalesced runs.
 // Records whose fine part lies beyond the local window (only when coarse parts are smaller
 // than a round) take a cursor each.
 __global__ void __launch_bounds__(SPLIT_THREADS, 1)
-    k_part_split2(const uint4* __restrict__ rec, const unsigned* __restrict__ total_ptr, int plog,
+    k_part_split(const uint4* __restrict__ rec, const unsigned* __restrict__ total_ptr, int plog,
                   unsigned* __restrict__ fine_fill, uint4* __restrict__ rec2) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int RI = 3 * PLACE_TRI;
@@ -1557,14 +1472,15 @@ struct fa_plan {
     int64_t nb;               // row buckets of BV vertices
     int plog, nparts;         // fine parts (sorted in shared memory)
     int plog_c, nparts_c;     // placement parts (== fine unless two_level)
-    bool two_level;           // coarse placement + k_part_split (more than SPLIT_MIN fine parts)
+    bool two_level;           // coarse placement + k_part_split (SPLIT_MIN fine parts or SPLIT_BYTES of records)
     int64_t chunk_place;
     int nblk_place;
     unsigned* part_off;       // nparts + 1 (fine)
     unsigned* part_off_c;     // nparts_c + 1 (== part_off unless two_level)
     unsigned* part_fill;      // nparts_c
-    bool fine_hist;           // two_level with the fine counts from k_part_hist (parallel k_part_split2)
-    unsigned* fine_fill;      // nparts (fine_hist): split cursors
+    bool fine_hist;           // == two_level: k_part_hist counts the fine parts (k_part_split cursors)
+    unsigned* fine_fill;      // nparts (two_level): split cursors
+    bool fine_global;         // fine counts by global atomics (more than FINE_HIST_MAX fine parts)
     unsigned* M;              // [nblk_place][nparts_c]
     uint4* rec;               // 3 * nme (owned incidences, grouped by placement part)
     uint4* rec2;              // two_level: regrouped by fine part
@@ -1660,9 +1576,10 @@ extern "C" int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t ro
     }
     p->nparts_c = int((nv + (int64_t(1) << p->plog_c) - 1) >> p->plog_c);
     if (p->nparts_c < 1) p->nparts_c = 1;
-    p->fine_hist = p->two_level && p->nparts <= FINE_HIST_MAX;
-    if (const char* env = getenv("FEMASM_B200_SPLIT1"))  // test hook: the one-block-per-coarse-part split
-        if (atoi(env) == 1) p->fine_hist = false;
+    p->fine_hist = p->two_level;
+    p->fine_global = p->two_level && p->nparts > FINE_HIST_MAX;
+    if (const char* env = getenv("FEMASM_B200_FINE_GLOBAL"))  // test hook: global fine counts
+        if (atoi(env) == 1 && p->two_level) p->fine_global = true;
     p->chunk_place = (nme + PLACE_BLOCKS_PER_SM * NUM_SMS_B200 - 1) / (PLACE_BLOCKS_PER_SM * NUM_SMS_B200);
     p->nblk_place = int((nme + p->chunk_place - 1) / p->chunk_place);
     p->ninc = -1;
@@ -1725,8 +1642,9 @@ extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, 
     P.part_off = p->part_off_c; P.part_fill = p->part_fill; P.M = p->M; P.rec = p->rec;
     P.skey = p->skey; P.sn1 = p->sn1; P.sn2 = p->sn2; P.ivptr = p->ivptr; P.res = d_res;
     P.plog_f = p->plog; P.nparts_f = p->nparts; P.fine_hist = p->fine_hist;
+    P.fine_global = p->fine_global;
     P.part_off_f = p->part_off; P.fine_fill = p->fine_fill;
-    const size_t hist_smem = sizeof(unsigned) * (p->fine_hist ? p->nparts : p->nparts_c);
+    const size_t hist_smem = sizeof(unsigned) * (P.fine_hist && !P.fine_global ? p->nparts : p->nparts_c);
     FA_CUDA(cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_smem)));
     k_part_hist<<<p->nblk_place, PLACE_THREADS, hist_smem, st>>>(P);
     FA_LAUNCH_CHECK("k_part_hist");
@@ -1739,21 +1657,14 @@ extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, 
     if (p->fine_hist) {
         constexpr int RI = 3 * PLACE_TRI;
         const size_t split_smem = size_t(RI) * (sizeof(uint4) + sizeof(unsigned short)) + sizeof(unsigned) * 3 * SPLIT2_LOCAL;
-        FA_CUDA(cudaFuncSetAttribute(k_part_split2, cudaFuncAttributeMaxDynamicSharedMemorySize, int(split_smem)));
+        FA_CUDA(cudaFuncSetAttribute(k_part_split, cudaFuncAttributeMaxDynamicSharedMemorySize, int(split_smem)));
         int nsm = 0, dev = 0;
         FA_CUDA(cudaGetDevice(&dev));
         FA_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         const int64_t rounds = (3 * p->nme + RI - 1) / RI;  // upper bound on the owned incidences
         const unsigned grid = unsigned(rounds < nsm ? rounds : nsm);
-        k_part_split2<<<grid, SPLIT_THREADS, split_smem, st>>>(p->rec, p->part_off + p->nparts, p->plog, p->fine_fill,
+        k_part_split<<<grid, SPLIT_THREADS, split_smem, st>>>(p->rec, p->part_off + p->nparts, p->plog, p->fine_fill,
                                                                p->rec2);
-        FA_LAUNCH_CHECK("k_part_split2");
-    } else if (p->two_level) {
-        const int F = 1 << (p->plog_c - p->plog);
-        const size_t split_smem = size_t(3 * PLACE_TRI) * (sizeof(uint4) + 1) + sizeof(unsigned) * 3 * F;
-        FA_CUDA(cudaFuncSetAttribute(k_part_split, cudaFuncAttributeMaxDynamicSharedMemorySize, int(split_smem)));
-        k_part_split<<<p->nparts_c, SPLIT_THREADS, split_smem, st>>>(p->rec, p->part_off_c, p->plog_c, p->plog,
-                                                                       p->part_off, p->nparts, p->rec2);
         FA_LAUNCH_CHECK("k_part_split");
     }
     P.plog = p->plog; P.nparts = p->nparts; P.part_off = p->part_off;  // sort level: fine parts

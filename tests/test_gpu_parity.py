@@ -249,15 +249,16 @@ def test_isolated_vertices_have_empty_rows():
         assert_same_csc(got, ref, kind)
 
 
-@pytest.mark.parametrize("split1", (0, 1))
-@pytest.mark.parametrize("coarse_log2", (11, 14))
+@pytest.mark.parametrize("fine_global", (0, 1))
+@pytest.mark.parametrize("coarse_log2", (11, 14, 18))
 @pytest.mark.parametrize("kind", KINDS)
-def test_two_level_plan(monkeypatch, kind, coarse_log2, split1):
+def test_two_level_plan(monkeypatch, kind, coarse_log2, fine_global):
     """Large row blocks place incidences by coarse part and regroup them by fine part
-    (k_part_split2, or with split1 the one-block-per-coarse-part k_part_split); forced here
-    on a small mesh and checked bitwise."""
+    (k_part_split); the fine counts come from k_part_hist's shared memory or (more than
+    49152 fine parts, forced with fine_global) from global atomics.  Forced here on a small
+    mesh and checked bitwise."""
     monkeypatch.setenv("FEMASM_B200_COARSE_LOG2", str(coarse_log2))
-    monkeypatch.setenv("FEMASM_B200_SPLIT1", str(split1))
+    monkeypatch.setenv("FEMASM_B200_FINE_GLOBAL", str(fine_global))
     sm = seeded_square_mesh(70, 4)  # 5041 vertices: 5 fine parts
     areas = fo.triangle_areas(sm.vertices, sm.connectivity)
     ref = c_oracle.assemble(kind, sm.vertices, sm.connectivity, areas, sm.weights, 1.5, 0.6)

@@ -1,5 +1,6 @@
 """Cold step through fa_plan_build + fa_assemble vs fa_assemble_cold, eager and graph-replayed
-(development tool): python tools/cold_time.py [CFG]"""
+(development tool): python tools/cold_time.py [CFG [G RANK]] - with G, RANK: that rank's row block
+of a G-way row-block decomposition (bench.py's split), timed alone on this GPU."""
 import sys
 from pathlib import Path
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
@@ -10,6 +11,8 @@ from paper_1305_3122_b200.device import ResultBlock
 from paper_1305_3122_b200.meshgen import seeded_square_mesh, BASELINE_CONFIGS
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
+G = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+rank = int(sys.argv[3]) if len(sys.argv) > 3 else 0
 kind, n, lam, mu = BASELINE_CONFIGS[cfg]
 sm = seeded_square_mesh(n, 0)
 dev = torch.device("cuda")
@@ -17,7 +20,10 @@ me = torch.from_numpy(sm.connectivity.astype(np.int32)).to(dev)
 q = torch.from_numpy(sm.vertices).to(dev)
 a = torch.from_numpy(fa.compute_areas(sm.vertices, sm.connectivity)).to(dev)
 w = torch.from_numpy(sm.weights).to(dev) if kind == "massw" else None
-plan = fa.AssemblyPlan(sm.nme, sm.nq)
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+from paper_1305_3122_b200.dist import row_blocks  # noqa: E402
+v0, v1 = row_blocks(sm.nq, G)[rank]
+plan = fa.AssemblyPlan(sm.nme, sm.nq, v0, v1)
 plan.build(me)
 cap = plan.capacity(kind)
 rowptr = torch.empty(plan.rows(kind) + 1, dtype=torch.int64, device=dev)
@@ -67,4 +73,5 @@ def timed(fn, graph, reps=30):
 for name, fn in (("build+assemble", split_step), ("assemble_cold", cold_step)):
     for graph in (False, True):
         t, nnz = timed(fn, graph)
-        print(f"{cfg} {name:16s} graph={graph!s:5s} {t:8.1f} us  nnz={nnz}  tri/s={sm.nme / (t * 1e-6):.3e}", flush=True)
+        print(f"{cfg} G={G} rank={rank} {name:16s} graph={graph!s:5s} {t:8.1f} us  nnz={nnz}  "
+              f"tri/s (this block's share of the mesh) {sm.nme / G / (t * 1e-6):.3e}", flush=True)
