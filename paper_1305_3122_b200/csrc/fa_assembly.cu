@@ -157,6 +157,10 @@ struct PlanArgs {
     unsigned* sn2;          // neighbour at corner a+2
     unsigned* ivptr;        // nv + 1: first incidence of every owned vertex
     fa_result* res;
+    // row blocks (multi-GPU): K1 compacts the triangles with an owned corner per block
+    // ({k, c0, c1, c2} at block * chunk ..), so K3 skips the others
+    uint4* tri;             // null for the whole mesh
+    unsigned* tri_cnt;      // per K1/K3 block
 };
 
 __device__ __forceinline__ bool tri_ids_valid(int c0, int c1, int c2, int64_t nq) {
@@ -172,7 +176,9 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
     // the coarse ones
     const bool fs = P.fine_hist && !P.fine_global;
     const int hlog = fs ? P.plog_f : P.plog, hn = fs ? P.nparts_f : P.nparts;
+    __shared__ unsigned s_tn;
     for (int i = threadIdx.x; i < hn; i += PLACE_THREADS) s_cnt[i] = 0;
+    if (threadIdx.x == 0) s_tn = 0;
     __syncthreads();
     const int64_t k0 = int64_t(blockIdx.x) * P.chunk, k1 = min(P.nme, k0 + P.chunk);
     constexpr int U = 4;  // triangles in flight per thread
@@ -190,6 +196,14 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
             // a triangle with an out-of-range corner is reported and left out entirely, so no
             // incidence ever names an invalid neighbour
             const bool ok = tri_ids_valid(c[u][0], c[u][1], c[u][2], P.nq);
+            if (P.tri && ok) {
+                bool own = false;
+#pragma unroll
+                for (int a = 0; a < 3; ++a) own |= c[u][a] >= P.v0 && c[u][a] < P.v1;
+                if (own)
+                    P.tri[k0 + atomicAdd(&s_tn, 1u)] =
+                        make_uint4(unsigned(k), unsigned(c[u][0]), unsigned(c[u][1]), unsigned(c[u][2]));
+            }
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 const int64_t v = c[u][a];
@@ -202,6 +216,7 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
         }
     }
     __syncthreads();
+    if (P.tri && threadIdx.x == 0) P.tri_cnt[blockIdx.x] = s_tn;
     unsigned* row = P.M + int64_t(blockIdx.x) * P.nparts;
     if (!P.fine_hist) {
         for (int i = threadIdx.x; i < P.nparts; i += PLACE_THREADS) {
@@ -278,33 +293,44 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
             s_cnt[i] = 0;
         }
     }
+    // this block's triangles: its chunk of the mesh, or (row blocks) the ones K1 compacted
+    const bool cmp = P.tri != nullptr;
+    const int64_t nj = cmp ? int64_t(P.tri_cnt[blockIdx.x]) : kb1 - kb0;
+    auto fetch = [&](int64_t j, unsigned& k, int (&c)[3]) {
+        c[0] = c[1] = c[2] = -1;
+        if (j >= nj) return;
+        if (cmp) {
+            const uint4 t = P.tri[kb0 + j];
+            k = t.x; c[0] = int(t.y); c[1] = int(t.z); c[2] = int(t.w);
+        } else {
+            k = unsigned(kb0 + j);
+            load_tri_ids(P.me, kb0 + j, c[0], c[1], c[2]);
+        }
+    };
     // triangle ids of the next round are loaded while the current one is placed
     int nxt[TPT][3];
+    unsigned nk[TPT];
 #pragma unroll
-    for (int t = 0; t < TPT; ++t) {
-        const int64_t k = kb0 + t * PLACE_THREADS + tid;
-        nxt[t][0] = nxt[t][1] = nxt[t][2] = -1;
-        if (k < kb1) load_tri_ids(P.me, k, nxt[t][0], nxt[t][1], nxt[t][2]);
-    }
-    for (int64_t r0 = kb0; r0 < kb1; r0 += PLACE_TRI) {
+    for (int t = 0; t < TPT; ++t) fetch(t * PLACE_THREADS + tid, nk[t], nxt[t]);
+    for (int64_t r0 = 0; r0 < nj; r0 += PLACE_TRI) {
         int cur[TPT][3];
+        unsigned ck[TPT];
 #pragma unroll
         for (int t = 0; t < TPT; ++t) {
             cur[t][0] = nxt[t][0];
             cur[t][1] = nxt[t][1];
             cur[t][2] = nxt[t][2];
-            const int64_t k = r0 + PLACE_TRI + t * PLACE_THREADS + tid;
-            nxt[t][0] = nxt[t][1] = nxt[t][2] = -1;
-            if (k < kb1) load_tri_ids(P.me, k, nxt[t][0], nxt[t][1], nxt[t][2]);
+            ck[t] = nk[t];
+            fetch(r0 + PLACE_TRI + t * PLACE_THREADS + tid, nk[t], nxt[t]);
         }
         __syncthreads();
         uint4 rec[3 * TPT];
         unsigned part[3 * TPT], rank[3 * TPT];
 #pragma unroll
         for (int t = 0; t < TPT; ++t) {
-            const int64_t k = r0 + t * PLACE_THREADS + tid;
+            const unsigned k = ck[t];
             const int c[3] = {cur[t][0], cur[t][1], cur[t][2]};
-            const bool ok = tri_ids_valid(c[0], c[1], c[2], P.nq);  // as k_part_hist
+            const bool ok = tri_ids_valid(c[0], c[1], c[2], P.nq);  // as k_part_hist (-1: no triangle)
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 const int64_t v = c[a];
@@ -1400,7 +1426,7 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const unsigned long lon
 constexpr int TRI_WT_U = FA_TRI_WT_U;  // triangles in flight per thread
 __global__ void __launch_bounds__(256) k_tri_wt(const int32_t* __restrict__ me, int64_t nme, int64_t nq,
                                                  const double* __restrict__ areas, const double* __restrict__ w,
-                                                 double4* __restrict__ Wt) {
+                                                 double4* __restrict__ Wt, int64_t v0, int64_t v1) {
     const uint64_t pol = l2_evict_first_policy();
     const uint64_t keep = l2_evict_last_policy();
     const int64_t k0 = int64_t(blockIdx.x) * (256 * TRI_WT_U) + threadIdx.x;
@@ -1409,6 +1435,7 @@ __global__ void __launch_bounds__(256) k_tri_wt(const int32_t* __restrict__ me, 
 #pragma unroll
     for (int u = 0; u < TRI_WT_U; ++u) {
         const int64_t k = k0 + u * 256;
+        c[u][0] = c[u][1] = c[u][2] = -1;
         if (k < nme) {
             c[u][0] = ld_stream_i32(me + 3 * k, pol);
             c[u][1] = ld_stream_i32(me + 3 * k + 1, pol);
@@ -1416,16 +1443,24 @@ __global__ void __launch_bounds__(256) k_tri_wt(const int32_t* __restrict__ me, 
             ar[u] = ld_stream_f64(areas + k, pol);
         }
     }
+    bool own[TRI_WT_U];  // row blocks: only triangles with a corner in [v0, v1) are gathered
+#pragma unroll
+    for (int u = 0; u < TRI_WT_U; ++u) {
+        bool any = false;
+#pragma unroll
+        for (int a = 0; a < 3; ++a) any |= c[u][a] >= v0 && c[u][a] < v1;
+        own[u] = k0 + u * 256 < nme && any;
+    }
 #pragma unroll
     for (int u = 0; u < TRI_WT_U; ++u)
-        if (k0 + u * 256 < nme)
+        if (own[u])
 #pragma unroll
             for (int a = 0; a < 3; ++a)  // out-of-range ids (reported by the plan build) read nothing
                 wc[u][a] = unsigned(c[u][a]) < nq ? ld_keep_f64(w + c[u][a], keep) : 0.0;
 #pragma unroll
     for (int u = 0; u < TRI_WT_U; ++u) {
         const int64_t k = k0 + u * 256;
-        if (k < nme) {
+        if (own[u]) {
             double4 r;
             r.x = ddiv_rcp(FMUL(wc[u][0], ar[u]), 30.0, FA_RCP30);
             r.y = ddiv_rcp(FMUL(wc[u][1], ar[u]), 30.0, FA_RCP30);
@@ -1481,6 +1516,8 @@ struct fa_plan {
     bool fine_hist;           // == two_level: k_part_hist counts the fine parts (k_part_split cursors)
     unsigned* fine_fill;      // nparts (two_level): split cursors
     bool fine_global;         // fine counts by global atomics (more than FINE_HIST_MAX fine parts)
+    uint4* tri;               // row blocks: triangles with an owned corner, compacted per K1 block
+    unsigned* tri_cnt;
     unsigned* M;              // [nblk_place][nparts_c]
     uint4* rec;               // 3 * nme (owned incidences, grouped by placement part)
     uint4* rec2;              // two_level: regrouped by fine part
@@ -1513,7 +1550,7 @@ static void plan_free(fa_plan* p) {
     if (p->ev_fork) cudaEventDestroy(p->ev_fork);
     if (p->ev_wt) cudaEventDestroy(p->ev_wt);
     if (p->ev_done) cudaEventDestroy(p->ev_done);
-    cudaFree(p->part_off); cudaFree(p->part_fill); cudaFree(p->fine_fill); cudaFree(p->M); cudaFree(p->rec); cudaFree(p->skey); cudaFree(p->sn1);
+    cudaFree(p->part_off); cudaFree(p->part_fill); cudaFree(p->fine_fill); cudaFree(p->tri); cudaFree(p->tri_cnt); cudaFree(p->M); cudaFree(p->rec); cudaFree(p->skey); cudaFree(p->sn1);
     cudaFree(p->sn2); cudaFree(p->ivptr); cudaFree(p->status);
     cudaFree(p->bsym); cudaFree(p->blen); cudaFree(p->bdrop); cudaFree(p->bshift); cudaFree(p->read_done);
     if (p->part_off_c != p->part_off) cudaFree(p->part_off_c);
@@ -1591,6 +1628,10 @@ extern "C" int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t ro
     if (e == cudaSuccess && p->two_level) e = cudaMalloc(&p->rec2, sizeof(uint4) * ninc_max);
     if (e == cudaSuccess) e = cudaMalloc(&p->part_fill, sizeof(unsigned) * p->nparts_c);
     if (e == cudaSuccess && p->fine_hist) e = cudaMalloc(&p->fine_fill, sizeof(unsigned) * p->nparts);
+    if (row_begin > 0 || row_end < nq) {  // row block: the placement visits only owning triangles
+        if (e == cudaSuccess) e = cudaMalloc(&p->tri, sizeof(uint4) * size_t(nme));
+        if (e == cudaSuccess) e = cudaMalloc(&p->tri_cnt, sizeof(unsigned) * size_t(p->nblk_place));
+    }
     if (e == cudaSuccess) e = cudaMalloc(&p->M, sizeof(unsigned) * size_t(p->nblk_place) * p->nparts_c);
     if (e == cudaSuccess) e = cudaMalloc(&p->rec, sizeof(uint4) * ninc_max);
     if (e == cudaSuccess) e = cudaMalloc(&p->skey, sizeof(unsigned) * ninc_max);
@@ -1643,6 +1684,7 @@ extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, 
     P.skey = p->skey; P.sn1 = p->sn1; P.sn2 = p->sn2; P.ivptr = p->ivptr; P.res = d_res;
     P.plog_f = p->plog; P.nparts_f = p->nparts; P.fine_hist = p->fine_hist;
     P.fine_global = p->fine_global;
+    P.tri = p->tri; P.tri_cnt = p->tri_cnt;
     P.part_off_f = p->part_off; P.fine_fill = p->fine_fill;
     const size_t hist_smem = sizeof(unsigned) * (P.fine_hist && !P.fine_global ? p->nparts : p->nparts_c);
     FA_CUDA(cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_smem)));
@@ -1717,7 +1759,7 @@ extern "C" int fa_plan_capacity(fa_plan* p, int kind, int64_t* capacity) {
 static int launch_tri_wt(fa_plan* p, const double* d_areas, const double* d_w, cudaStream_t st) {
     if (!p->Wt) FA_CUDA(cudaMalloc(&p->Wt, sizeof(double4) * size_t(p->nme)));
     k_tri_wt<<<unsigned((p->nme + 256 * TRI_WT_U - 1) / (256 * TRI_WT_U)), 256, 0, st>>>(p->me, p->nme, p->nq, d_areas,
-                                                                                       d_w, p->Wt);
+                                                                                       d_w, p->Wt, p->v0, p->v1);
     FA_LAUNCH_CHECK("k_tri_wt");
     return FA_OK;
 }
