@@ -302,23 +302,29 @@ def test_vertex_above_bucket_capacity(kind):
     assert_same_csc(got, ref, f"{kind} hub 1300")
 
 
+@pytest.mark.parametrize("block", (None, 0, 1))
 @pytest.mark.parametrize("kind", KINDS)
-def test_assemble_cold_entry_point(kind):
-    """fa_assemble_cold (plan build + numeric pass in one call, the weighted mass's triangle
-    records on a side stream) equals the oracle bitwise, repeatedly and after a plain
-    fa_assemble on the same plan (the prepared records are consumed once)."""
+def test_assemble_cold_entry_point(kind, block):
+    """fa_assemble_cold (plan build + numeric pass in one call; the weighted mass's triangle
+    records on a side stream, or for a row block from the plan's first pass) equals the
+    oracle bitwise, repeatedly and after a plain fa_assemble on the same plan (the prepared
+    records are consumed once)."""
     import torch
     from paper_1305_3122_b200.device import ResultBlock
 
     sm = seeded_square_mesh(64, 5)
     areas = fo.triangle_areas(sm.vertices, sm.connectivity)
-    ref = c_oracle.assemble(kind, sm.vertices, sm.connectivity, areas, sm.weights, 1.0, 0.5)
+    v0, v1 = (0, sm.nq) if block is None else [(0, sm.nq // 3), (sm.nq // 3, sm.nq)][block]
+    if block is None:
+        ref = c_oracle.assemble(kind, sm.vertices, sm.connectivity, areas, sm.weights, 1.0, 0.5)
+    else:
+        ref = fo.assemble_row_block(kind, sm.vertices, sm.connectivity, areas, sm.weights, 1.0, 0.5, v0, v1)
     dev = torch.device("cuda")
     me = torch.from_numpy(np.ascontiguousarray(sm.connectivity, dtype=np.int32)).to(dev)
     q = torch.from_numpy(sm.vertices).to(dev)
     a = torch.from_numpy(areas).to(dev)
     w = torch.from_numpy(sm.weights).to(dev)
-    plan = fa.AssemblyPlan(sm.nme, sm.nq)
+    plan = fa.AssemblyPlan(sm.nme, sm.nq, v0, v1)
     plan.build(me)
     cap = plan.capacity(kind)
     rowptr = torch.empty(plan.rows(kind) + 1, dtype=torch.int64, device=dev)
