@@ -955,6 +955,78 @@ __device__ __forceinline__ void row_keys(const BucketRecs& R, int start, int deg
     sort16(sk);
 }
 
+// Scalar kinds, fast row: the row's entries in column order from its sorted candidate keys -
+// every position summed sequentially in ascending k (the slot order inside a run of equal
+// columns), the diagonal (all incidences, ascending k) inserted before the first larger
+// column - written to col/val[0..]; CHECK: only the first `room` entries are stored.  Exact-zero
+// sums stay as entries (k_compact removes them) and are counted; returns that count.
+template <int KIND, bool CHECK>
+__device__ __forceinline__ int64_t walk_row(const BucketRecs& R, const unsigned (&sk)[2 * MAXD], int start, int deg,
+                                            unsigned vv, int32_t* col, double* val, int64_t room) {
+    constexpr int CAP = KindTraits<KIND>::CAP;
+    double dsum = 0.0;
+#pragma unroll
+    for (int i = 0; i < MAXD; ++i)
+        if (i < deg) dsum = FADD(dsum, R.vals[start + i]);
+    int64_t zeros = 0;
+    int o = 0;
+    auto emit = [&](unsigned c, double x) {
+        if (!CHECK || o < room) {
+            col[o] = int32_t(c);
+            val[o] = x;
+        }
+        zeros += x == 0.0 ? 1 : 0;
+        ++o;
+    };
+    unsigned prev = 0xffffffffu;
+    double sum = 0.0;
+    bool diag = false;
+#pragma unroll
+    for (int j = 0; j <= 2 * MAXD; ++j) {
+        const unsigned key = j < 2 * MAXD ? sk[j] : 0xffffffffu;
+        const unsigned c = key == 0xffffffffu ? 0xffffffffu : (key >> 4);
+        if (c != prev) {
+            if (prev != 0xffffffffu) emit(prev, sum);
+            if (!diag && vv < c) {
+                emit(vv, dsum);
+                diag = true;
+            }
+            sum = 0.0;
+            prev = c;
+        }
+        if (j < 2 * MAXD && c != 0xffffffffu) {
+            const int sl = int(key & 15);
+            sum = FADD(sum, R.vals[(1 + (sl & 1)) * CAP + start + (sl >> 1)]);
+        }
+    }
+    return zeros;
+}
+
+// A bucket's staged CSR segment -> global memory with 16-byte stores: columns in fours,
+// values in pairs, after a scalar head that brings the global position to 16-byte alignment
+// (the staging is read with scalar loads).
+template <int NT>
+__device__ __forceinline__ void copy_out(const int32_t* st_col, const double* st_val, int32_t* gcol, double* gval,
+                                         int tot, uint64_t pol) {
+    const int tid = threadIdx.x;
+    const unsigned ac = unsigned(reinterpret_cast<uintptr_t>(gcol)) & 15u;
+    const unsigned av = unsigned(reinterpret_cast<uintptr_t>(gval)) & 15u;
+    const int hc = min(tot, int(((16u - ac) & 15u) >> 2)), hv = min(tot, int(((16u - av) & 15u) >> 3));
+    if (tid < hc) st_stream_i32(gcol + tid, st_col[tid], pol);
+    if (tid < hv) st_stream_f64(gval + tid, st_val[tid], pol);
+    for (int e = hc + 4 * tid; e < tot; e += 4 * NT) {
+        if (e + 3 < tot) {
+            st_stream_i32x4(gcol + e, st_col[e], st_col[e + 1], st_col[e + 2], st_col[e + 3], pol);
+        } else {
+            for (int j = e; j < tot; ++j) st_stream_i32(gcol + j, st_col[j], pol);
+        }
+    }
+    for (int e = hv + 2 * tid; e < tot; e += 2 * NT) {
+        if (e + 1 < tot) st_stream_f64x2(gval + e, st_val[e], st_val[e + 1], pol);
+        else st_stream_f64(gval + e, st_val[e], pol);
+    }
+}
+
 template <int KIND>
 __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::MIN_BLOCKS)
     k_rows(const __grid_constant__ RowsArgs A) {
@@ -992,9 +1064,11 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     const unsigned gbase = A.ivptr[vb0];
     for (int i = tid; i <= BV; i += NT) s_vst[i] = int(A.ivptr[vb0 + min(i, nvb)] - gbase);
     const int64_t vbase = A.v0 + vb0;
+    // own coordinates: gradients, or the area when none is given (the weighted mass never reads q)
+    const bool need_q = KIND == FA_KIND_STIFF || KIND == FA_KIND_ELASTIC || (KIND == FA_KIND_MASS && !A.areas);
     for (int i = tid; i < BV; i += NT) {
         const int64_t vv = vbase + i;
-        s_oq[i] = (A.q && vv < A.v1) ? A.q[vv] : make_double2(0.0, 0.0);
+        s_oq[i] = (need_q && A.q && vv < A.v1) ? A.q[vv] : make_double2(0.0, 0.0);
         s_ow[i] = 0.0;  // (the weighted mass reads its W per triangle, k_tri_wt)
     }
     __syncthreads();
@@ -1096,9 +1170,47 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     __syncthreads();
     TL(b, 2);
 
+    int64_t zeros = 0;
+    uint64_t base = 0;
+    if constexpr (EARLY) {
+        // ---- c+d) scalar kinds: each fast row walks its sorted columns once, summing every
+        //      position sequentially in ascending k and writing it with its column straight
+        //      into the compact staging.  The staging lies in the plan-entry arrays, dead once
+        //      phase a is done (n1 + n2 + ka hold 12 bytes per incidence slot, a staged entry
+        //      is 12 bytes), so the records' values stay intact for the unstaged fallback.
+        const bool staged = !__syncthreads_or(slow) && total <= CAP;
+        double* sv = reinterpret_cast<double*>(R.n1);    // [CAP], spans n1 and n2
+        int32_t* sc = reinterpret_cast<int32_t*>(R.ka);  // [CAP]
+        if (staged && fast) zeros = walk_row<KIND, false>(R, sk, start, deg, vv, sc + excl, sv + excl, 0);
+        base = lookback_wait(A.status, b, uint64_t(total), &s_prefix);  // ends with a barrier
+        TL(b, 4);
+        if (active) st_stream_i64(A.rowptr + r, int64_t(base) + excl, pol_first);
+        if (active && r == A.nrows - 1) {
+            A.rowptr[A.nrows] = int64_t(base) + excl + count;
+            A.res->nnz = int64_t(base) + excl + count;
+        }
+        if (slow) atomicAdd(reinterpret_cast<unsigned long long*>(&A.res->heavy_rows), 1ull);
+        if (staged && int64_t(base) + total <= A.capacity) {
+            copy_out<NT>(sc, sv, A.col + base, A.val + base, int(total), pol_first);
+        } else if (staged) {
+            for (int64_t e = tid; e < total; e += NT) {
+                const int64_t g = int64_t(base) + e;
+                if (g < A.capacity) {
+                    st_stream_i32(A.col + g, sc[e], pol_first);
+                    st_stream_f64(A.val + g, sv[e], pol_first);
+                }
+            }
+        } else {
+            const int64_t o = int64_t(base) + excl;
+            if (fast) zeros = walk_row<KIND, true>(R, sk, start, deg, vv, A.col + o, A.val + o, A.capacity - o);
+            if (slow)
+                zeros = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc],
+                                          s_ow[vloc], s, o, true, true, true)
+                            .zeros;
+        }
+    } else {
     // ---- c) per row: each position summed sequentially in ascending k (== stable argsort +
     //         bincount of the reference); exact-zero sums stay as entries and are counted
-    int64_t zeros = 0;
     double dsum[NV], run_val[NC + 1][NV];
     int diag_at = -1;  // the diagonal is emitted right after run j == diag_at
 #pragma unroll
@@ -1199,7 +1311,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
             }
         }
     }
-    const uint64_t base = lookback_wait(A.status, b, uint64_t(total), &s_prefix);  // ends with a barrier
+    base = lookback_wait(A.status, b, uint64_t(total), &s_prefix);  // ends with a barrier
     TL(b, 4);
     if (active) st_stream_i64(A.rowptr + r, int64_t(base) + excl, pol_first);
     if (active && r == A.nrows - 1) {
@@ -1207,7 +1319,9 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         A.res->nnz = int64_t(base) + excl + count;
     }
     if (slow) atomicAdd(reinterpret_cast<unsigned long long*>(&A.res->heavy_rows), 1ull);
-    if (staged) {
+    if (staged && int64_t(base) + total <= A.capacity) {
+        copy_out<NT>(st_col, st_val, A.col + base, A.val + base, int(total), pol_first);
+    } else if (staged) {
         for (int64_t e = tid; e < total; e += NT) {
             const int64_t g = int64_t(base) + e;
             if (g < A.capacity) {
@@ -1256,6 +1370,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
             if (EARLY) zeros = rc.zeros;
         }
     }
+    }  // !EARLY
     // zero sums of the bucket -> compaction data (k_compact runs only when some exist)
     block_exclusive_scan<NT>(zeros, s_warp, &s_total);
     const unsigned bz = unsigned(s_total);

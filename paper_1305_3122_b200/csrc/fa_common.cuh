@@ -83,6 +83,17 @@ __device__ __forceinline__ void st_stream_i64(int64_t* p, int64_t v, uint64_t po
 __device__ __forceinline__ void st_stream_f64(double* p, double v, uint64_t pol) {
     asm volatile("st.global.L1::no_allocate.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v), "l"(pol) : "memory");
 }
+// 16-byte stores (p 16-byte aligned)
+__device__ __forceinline__ void st_stream_f64x2(double* p, double x, double y, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(x), "d"(y),
+                 "l"(pol)
+                 : "memory");
+}
+__device__ __forceinline__ void st_stream_i32x4(int* p, int x, int y, int z, int w, uint64_t pol) {
+    asm volatile("st.global.L1::no_allocate.L2::cache_hint.v4.s32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(p), "r"(x),
+                 "r"(y), "r"(z), "r"(w), "l"(pol)
+                 : "memory");
+}
 
 // Randomly gathered arrays (areas, q, w) are pulled into L2 once, sequentially, with an
 // evict-last priority, and gathered with the same priority: every later random access hits L2
