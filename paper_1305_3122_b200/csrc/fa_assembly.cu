@@ -515,6 +515,21 @@ __device__ void sort_incidences(unsigned* key, unsigned* n1, unsigned* n2, int d
     }
 }
 
+// 8 keys ascending (19 comparators, verified by the 0-1 principle)
+__device__ __forceinline__ void sort8(unsigned (&k)[8]) {
+    auto cx = [](unsigned& x, unsigned& y) {
+        const unsigned lo = min(x, y), hi = max(x, y);
+        x = lo;
+        y = hi;
+    };
+    cx(k[0], k[2]); cx(k[1], k[3]); cx(k[4], k[6]); cx(k[5], k[7]);
+    cx(k[0], k[4]); cx(k[1], k[5]); cx(k[2], k[6]); cx(k[3], k[7]);
+    cx(k[0], k[1]); cx(k[2], k[3]); cx(k[4], k[5]); cx(k[6], k[7]);
+    cx(k[2], k[4]); cx(k[3], k[5]);
+    cx(k[1], k[4]); cx(k[3], k[6]);
+    cx(k[1], k[2]); cx(k[3], k[4]); cx(k[5], k[6]);
+}
+
 // K4: one block per part.  Counting sort by vertex, every vertex's list by k; SoA output and
 // per-vertex offsets.  Parts of PV == 1024 vertices and up to SORT_CAP incidences are sorted
 // in shared memory, others in place in global memory.  s_cur[v]: count, then start, then
@@ -590,10 +605,22 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_cons
     __syncthreads();
     if (fast) {
         // per vertex: rank of every incidence among the vertex's keys (unique) -> source slot
-        // of every sorted position; then one coalesced permuting copy
+        // of every sorted position; then one coalesced permuting copy.  pack: k << 5 fits 32
+        // bits (k < 2^27), so the list position rides in the key's low bits
+        const bool pack = P.nme <= (int64_t(1) << 27);
         for (int v = tid; v < PV; v += SORT_THREADS) {
         const unsigned st = v ? s_cur[v - 1] : 0u, d = s_cur[v] - st;
-        if (d <= 8) {
+        if (d <= 8 && pack) {
+            // keys (k << 2 | a, unique) with the list position in three low bits, sorted by a
+            // 19-comparator network: the sorted position's source slot is in the low bits
+            unsigned kk[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) kk[j] = j < int(d) ? (key[st + j] << 3) | unsigned(j) : 0xffffffffu;
+            sort8(kk);
+#pragma unroll
+            for (int r = 0; r < 8; ++r)
+                if (r < int(d)) s_src[st + r] = (unsigned short)(st + (kk[r] & 7u));
+        } else if (d <= 8) {
             unsigned kk[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) kk[j] = j < int(d) ? key[st + j] : 0xffffffffu;
@@ -1182,6 +1209,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         double* sv = reinterpret_cast<double*>(R.n1);    // [CAP], spans n1 and n2
         int32_t* sc = reinterpret_cast<int32_t*>(R.ka);  // [CAP]
         if (staged && fast) zeros = walk_row<KIND, false>(R, sk, start, deg, vv, sc + excl, sv + excl, 0);
+        TL(b, 3);
         base = lookback_wait(A.status, b, uint64_t(total), &s_prefix);  // ends with a barrier
         TL(b, 4);
         if (active) st_stream_i64(A.rowptr + r, int64_t(base) + excl, pol_first);
