@@ -100,6 +100,7 @@ constexpr int SORT_CAP = 7680;     // part incidences sorted in shared memory (2
 // Resets the result block and zeroes the counters the following kernels accumulate into
 // (grid-stride; replaces separate memsets).
 __global__ void k_reset(fa_result* r, unsigned* z32, int64_t n32, uint64_t* z64, int64_t n64) {
+    pdl_enter();
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n32; i += stride) z32[i] = 0;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n64; i += stride) z64[i] = 0;
@@ -170,6 +171,7 @@ __device__ __forceinline__ bool tri_ids_valid(int c0, int c1, int c2, int64_t nq
 // K1: owned incidences per (block, part) and per part; index validation (sparse.py:131-137 semantics: first bad
 // position in the flattened connectivity).
 __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_constant__ PlanArgs P) {
+    pdl_enter();
     extern __shared__ unsigned s_cnt[];
     // counted per fine part in a two-level plan (the coarse counts are their sums); beyond
     // FINE_HIST_MAX fine parts the fine counts go to global memory and shared memory keeps
@@ -241,6 +243,7 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
 // fine counts (K1 fine_hist): the fine offsets, the split cursors, and the coarse offsets and
 // placement cursors taken at the coarse boundaries.
 __global__ void __launch_bounds__(PLAN_THREADS) k_part_scan(const __grid_constant__ PlanArgs P) {
+    pdl_enter();
     __shared__ unsigned s_warp[PLAN_THREADS / 32];
     __shared__ unsigned s_total;
     unsigned* cnt = P.fine_hist ? P.part_off_f : P.part_off;
@@ -273,6 +276,7 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_part_scan(const __grid_constan
 // are ranked by part in shared memory, staged in part order and written as coalesced runs.
 // Order inside a part is arbitrary (K4 sorts).
 __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_place(const __grid_constant__ PlanArgs P) {
+    pdl_enter();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int RI = 3 * PLACE_TRI;                  // incidences per round
     constexpr int TPT = PLACE_TRI / PLACE_THREADS;      // triangles per thread per round
@@ -399,6 +403,7 @@ constexpr int SPLIT_THREADS = 1024;
 __global__ void __launch_bounds__(SPLIT_THREADS, 1)
     k_part_split(const uint4* __restrict__ rec, const unsigned* __restrict__ total_ptr, int plog,
                   unsigned* __restrict__ fine_fill, uint4* __restrict__ rec2) {
+    pdl_enter();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int RI = 3 * PLACE_TRI;
     constexpr int PER = RI / SPLIT_THREADS;
@@ -535,6 +540,7 @@ __device__ __forceinline__ void sort8(unsigned (&k)[8]) {
 // in shared memory, others in place in global memory.  s_cur[v]: count, then start, then
 // (after placement) end of vertex v.
 __global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_constant__ PlanArgs P) {
+    pdl_enter();
     extern __shared__ __align__(16) unsigned s_dyn[];
     __shared__ unsigned s_warp[SORT_THREADS / 32];
     __shared__ unsigned s_total;
@@ -1057,6 +1063,7 @@ __device__ __forceinline__ void copy_out(const int32_t* st_col, const double* st
 template <int KIND>
 __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::MIN_BLOCKS)
     k_rows(const __grid_constant__ RowsArgs A) {
+    pdl_enter();
     using TR = KindTraits<KIND>;
     constexpr int NV = TR::NV, RPV = TR::RPV, NT = TR::THREADS, RVALS = TR::RVALS;
     constexpr int NC = 2 * MAXD;
@@ -1430,6 +1437,7 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const unsigned long lon
                                                           int64_t rows_per_bucket, int64_t nrows,
                                                           int64_t* __restrict__ rowptr, int32_t* col, double* val,
                                                           fa_result* res, unsigned* scan_ready) {
+    pdl_enter();
     extern __shared__ __align__(16) unsigned char cmp_raw[];
     double* s_v = reinterpret_cast<double*>(cmp_raw);            // [CMP_CAP]
     int32_t* s_c = reinterpret_cast<int32_t*>(s_v + CMP_CAP);     // [CMP_CAP]
@@ -1633,8 +1641,7 @@ static int launch_rows(const RowsArgs& A, int64_t nbuckets, cudaStream_t st) {
     const size_t smem = rows_smem_bytes<KIND>();
     FA_CUDA(cudaFuncSetAttribute(k_rows<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     if (g_timer_begin && record_timer(g_timer_begin, st) != FA_OK) return FA_ERR_CUDA;
-    k_rows<KIND><<<dim3(unsigned(nbuckets)), KindTraits<KIND>::THREADS, smem, st>>>(A);
-    FA_LAUNCH_CHECK("k_rows");
+    FA_CUDA(launch_pdl(7, k_rows<KIND>, dim3(unsigned(nbuckets)), dim3(KindTraits<KIND>::THREADS), smem, st, A));
     if (g_timer_end && record_timer(g_timer_end, st) != FA_OK) return FA_ERR_CUDA;
     return FA_OK;
 }
@@ -1806,7 +1813,16 @@ extern "C" int fa_plan_destroy(fa_plan* p) {
     return FA_OK;
 }
 
+// pdl: the plan kernels are launched as programmatic dependents of each other (see
+// launch_pdl); fa_assemble_cold turns it off while the W records run on a side stream, whose
+// blocks fill the SMs the plan kernels' tails leave idle.
+static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* stream, bool pdl);
+
 extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* stream) {
+    return plan_build(p, d_me, d_res, stream, true);
+}
+
+static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* stream, bool pdl) {
     if (!p || !d_me || !d_res) { set_error("fa_plan_build: NULL argument"); return FA_ERR_ARGUMENT; }
     cudaStream_t st = as_stream(stream);
     p->ninc = -1;
@@ -1817,9 +1833,12 @@ extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, 
     }
     p->me = d_me;
     // result + the part counts K1 accumulates (fine ones when it counts fine parts)
-    if (p->fine_hist) k_reset<<<8, 256, 0, st>>>(d_res, p->part_off, p->nparts + 1, nullptr, 0);
-    else k_reset<<<4, 256, 0, st>>>(d_res, p->part_off_c, p->nparts_c + 1, nullptr, 0);
-    FA_LAUNCH_CHECK("k_reset");
+    if (p->fine_hist)
+        FA_CUDA(launch_pdl(pdl ? 0 : -1, k_reset, dim3(8), dim3(256), 0, st, d_res, p->part_off, int64_t(p->nparts + 1),
+                           (uint64_t*)nullptr, int64_t(0)));
+    else
+        FA_CUDA(launch_pdl(pdl ? 0 : -1, k_reset, dim3(4), dim3(256), 0, st, d_res, p->part_off_c, int64_t(p->nparts_c + 1),
+                           (uint64_t*)nullptr, int64_t(0)));
     PlanArgs P;  // placement level (coarse parts when two_level)
     P.me = d_me; P.nme = p->nme; P.nq = p->nq; P.v0 = p->v0; P.v1 = p->v1;
     P.plog = p->plog_c; P.nparts = p->nparts_c; P.chunk = p->chunk_place;
@@ -1831,14 +1850,11 @@ extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, 
     P.part_off_f = p->part_off; P.fine_fill = p->fine_fill;
     const size_t hist_smem = sizeof(unsigned) * (P.fine_hist && !P.fine_global ? p->nparts : p->nparts_c);
     FA_CUDA(cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_smem)));
-    k_part_hist<<<p->nblk_place, PLACE_THREADS, hist_smem, st>>>(P);
-    FA_LAUNCH_CHECK("k_part_hist");
-    k_part_scan<<<1, PLAN_THREADS, 0, st>>>(P);
-    FA_LAUNCH_CHECK("k_part_scan");
+    FA_CUDA(launch_pdl(pdl ? 1 : -1, k_part_hist, dim3(p->nblk_place), dim3(PLACE_THREADS), hist_smem, st, P));
+    FA_CUDA(launch_pdl(pdl ? 2 : -1, k_part_scan, dim3(1), dim3(PLAN_THREADS), 0, st, P));
     const size_t place_smem = place_smem_bytes(p->nparts_c);
     FA_CUDA(cudaFuncSetAttribute(k_part_place, cudaFuncAttributeMaxDynamicSharedMemorySize, int(place_smem)));
-    k_part_place<<<p->nblk_place, PLACE_THREADS, place_smem, st>>>(P);
-    FA_LAUNCH_CHECK("k_part_place");
+    FA_CUDA(launch_pdl(pdl ? 3 : -1, k_part_place, dim3(p->nblk_place), dim3(PLACE_THREADS), place_smem, st, P));
     if (p->fine_hist) {
         constexpr int RI = 3 * PLACE_TRI;
         const size_t split_smem = size_t(RI) * (sizeof(uint4) + sizeof(unsigned short)) + sizeof(unsigned) * 3 * SPLIT2_LOCAL;
@@ -1848,16 +1864,14 @@ extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, 
         FA_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         const int64_t rounds = (3 * p->nme + RI - 1) / RI;  // upper bound on the owned incidences
         const unsigned grid = unsigned(rounds < nsm ? rounds : nsm);
-        k_part_split<<<grid, SPLIT_THREADS, split_smem, st>>>(p->rec, p->part_off + p->nparts, p->plog, p->fine_fill,
-                                                               p->rec2);
-        FA_LAUNCH_CHECK("k_part_split");
+        FA_CUDA(launch_pdl(pdl ? 4 : -1, k_part_split, dim3(grid), dim3(SPLIT_THREADS), split_smem, st, p->rec,
+                           p->part_off + p->nparts, p->plog, p->fine_fill, p->rec2));
     }
     P.plog = p->plog; P.nparts = p->nparts; P.part_off = p->part_off;  // sort level: fine parts
     P.rec = p->two_level ? p->rec2 : p->rec;
     const size_t sort_smem = sort_smem_bytes(p->plog);
     FA_CUDA(cudaFuncSetAttribute(k_part_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sort_smem)));
-    k_part_sort<<<p->nparts, SORT_THREADS, sort_smem, st>>>(P);
-    FA_LAUNCH_CHECK("k_part_sort");
+    FA_CUDA(launch_pdl(pdl ? 5 : -1, k_part_sort, dim3(p->nparts), dim3(SORT_THREADS), sort_smem, st, P));
     return FA_OK;
 }
 
@@ -1926,9 +1940,8 @@ extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double
     }
     // result block, look-back status (nb), the row-kernel and compaction tickets and the
     // compaction's scan flag (p->status has nb + 4 words)
-    k_reset<<<unsigned((p->nb + 4 + 255) / 256 < 64 ? (p->nb + 4 + 255) / 256 : 64), 256, 0, st>>>(
-        d_res, nullptr, 0, p->status, p->nb + 4);
-    FA_LAUNCH_CHECK("k_reset");
+    FA_CUDA(launch_pdl(6, k_reset, dim3(unsigned((p->nb + 4 + 255) / 256 < 64 ? (p->nb + 4 + 255) / 256 : 64)), dim3(256),
+                       0, st, d_res, (unsigned*)nullptr, int64_t(0), p->status, int64_t(p->nb + 4)));
     RowsArgs A;
     A.skey = p->skey; A.sn1 = p->sn1; A.sn2 = p->sn2; A.ivptr = p->ivptr;
     A.q = reinterpret_cast<const double2*>(d_q); A.w = d_w; A.areas = d_areas;
@@ -1962,11 +1975,9 @@ extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double
     const size_t cmp_smem = size_t(CMP_CAP) * (sizeof(double) + sizeof(int32_t));
     FA_CUDA(cudaFuncSetAttribute(k_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cmp_smem)));
     const unsigned cgrid = unsigned(p->nb < 2 * NUM_SMS_B200 ? p->nb : 2 * NUM_SMS_B200);
-    k_compact<<<cgrid, CMP_THREADS, cmp_smem, st>>>(p->bsym, p->blen, p->bdrop, p->bshift, p->read_done,
-                                                     reinterpret_cast<unsigned long long*>(p->status + p->nb + 1), p->nb,
-                                                     rpb, nrows, d_rowptr, d_col, d_val, d_res,
-                                                     reinterpret_cast<unsigned*>(p->status + p->nb + 2));
-    FA_LAUNCH_CHECK("k_compact");
+    FA_CUDA(launch_pdl(8, k_compact, dim3(cgrid), dim3(CMP_THREADS), cmp_smem, st, p->bsym, p->blen, p->bdrop, p->bshift,
+                       p->read_done, reinterpret_cast<unsigned long long*>(p->status + p->nb + 1), int64_t(p->nb), rpb,
+                       nrows, d_rowptr, d_col, d_val, d_res, reinterpret_cast<unsigned*>(p->status + p->nb + 2)));
     return FA_OK;
 }
 
@@ -1998,7 +2009,7 @@ extern "C" int fa_assemble_cold(fa_plan* p, const int32_t* d_me, int kind, const
     FA_CUDA(cudaEventRecord(p->ev_fork, st));
     FA_CUDA(cudaStreamWaitEvent(p->s_hi, p->ev_fork, 0));
     FA_CUDA(cudaStreamWaitEvent(p->s_lo, p->ev_fork, 0));
-    int rc = fa_plan_build(p, d_me, d_build_result, p->s_hi);
+    int rc = plan_build(p, d_me, d_build_result, p->s_hi, false);
     if (rc != FA_OK) return rc;
     rc = launch_tri_wt(p, d_areas, d_w, p->s_lo);
     if (rc != FA_OK) return rc;

@@ -1,6 +1,7 @@
 // Host-side error state and small C-ABI utilities of femasm_b200.
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "fa_common.cuh"
@@ -13,6 +14,14 @@ void set_error(const char* fmt, ...) {
     va_start(ap, fmt);
     vsnprintf(g_error, sizeof(g_error), fmt, ap);
     va_end(ap);
+}
+
+int pdl_mask() {
+    static const int mask = [] {
+        const char* env = getenv("FEMASM_B200_PDL_MASK");
+        return env ? int(strtol(env, nullptr, 0)) : 0x1bf;
+    }();
+    return mask;
 }
 
 int cuda_status(cudaError_t e, const char* what) {

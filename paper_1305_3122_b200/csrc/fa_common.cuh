@@ -30,6 +30,40 @@ int cuda_status(cudaError_t e, const char* what);
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// ---- programmatic dependent launch ----------------------------------------------------
+// The kernels of one assembly run back to back on a stream.  Each is launched with
+// programmatic stream serialization and starts with pdl_enter(): it lets the next kernel's
+// blocks be scheduled as soon as all of its own blocks have started (they occupy the SMs this
+// grid's tail leaves idle), then waits until the previous grid has completed and its memory is
+// visible.  Nothing is read or written before the wait, so stream order semantics are kept.
+__device__ __forceinline__ void pdl_enter() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+}
+
+// Launch sites that use PDL, one bit per site (0 plan reset, 1 hist, 2 scan, 3 place, 4 split,
+// 5 sort, 6 row reset, 7 rows, 8 compact; site < 0: never).  Site 6 is off: the row kernel's
+// blocks would otherwise be placed on SMs still configured for the part sort's shared-memory
+// carve-out, leaving them a small L1 for the whole kernel (C3 cold step +30 %).
+// FEMASM_B200_PDL_MASK overrides (experiments).
+int pdl_mask();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(int site, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = site >= 0 ? (pdl_mask() >> site) & 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 inline int grid_for(int64_t n, int block, int per_sm = 8) {
     int64_t want = (n + block - 1) / block;
     int64_t cap = int64_t(NUM_SMS_B200) * per_sm;
