@@ -859,7 +859,7 @@ __device__ __forceinline__ double record_entry(const RowsArgs& A, const double* 
     if constexpr (KIND == FA_KIND_ELASTIC) {
         return vals[(s * 6 + rel * 2 + t) * CAP + slot];
     } else {
-        return vals[rel * CAP + slot];
+        return rel == 0 ? vals[slot] : vals[CAP + 2 * slot + rel - 1];  // rel 1, 2 interleaved
     }
 }
 
@@ -910,7 +910,9 @@ __device__ __noinline__ RowCount general_row(const RowsArgs& A, BucketRecs R, bo
             n1 = R.n1[slot];
             n2 = R.n2[slot];
             if (need_vals)
-                for (int j = 0; j < RVALS; ++j) rv[j] = R.vals[j * KindTraits<KIND>::CAP + slot];
+                for (int j = 0; j < RVALS; ++j)
+                    rv[j] = KIND == FA_KIND_ELASTIC ? R.vals[j * KindTraits<KIND>::CAP + slot]
+                                                    : record_entry<KIND>(A, R.vals, slot, a, 0, j, 0);
             return;
         }
         const unsigned ka = A.skey[gfirst + i];
@@ -990,46 +992,45 @@ __device__ __forceinline__ void row_keys(const BucketRecs& R, int start, int deg
 
 // Scalar kinds, fast row: the row's entries in column order from its sorted candidate keys -
 // every position summed sequentially in ascending k (the slot order inside a run of equal
-// columns), the diagonal (all incidences, ascending k) inserted before the first larger
-// column - written to col/val[0..]; CHECK: only the first `room` entries are stored.  Exact-zero
+// columns), the diagonal (all incidences, ascending k) at position dpos (the columns below
+// it) - written to col/val[0..]; CHECK: only the first `room` entries are stored.  Exact-zero
 // sums stay as entries (k_compact removes them) and are counted; returns that count.
 template <int KIND, bool CHECK>
 __device__ __forceinline__ int64_t walk_row(const BucketRecs& R, const unsigned (&sk)[2 * MAXD], int start, int deg,
-                                            unsigned vv, int32_t* col, double* val, int64_t room) {
+                                            unsigned vv, int dpos, int32_t* col, double* val, int64_t room) {
     constexpr int CAP = KindTraits<KIND>::CAP;
+    const double* v12 = R.vals + CAP + 2 * start;  // (n1, n2) values of the row's incidences
     double dsum = 0.0;
 #pragma unroll
     for (int i = 0; i < MAXD; ++i)
         if (i < deg) dsum = FADD(dsum, R.vals[start + i]);
     int64_t zeros = 0;
-    int o = 0;
-    auto emit = [&](unsigned c, double x) {
-        if (!CHECK || o < room) {
-            col[o] = int32_t(c);
-            val[o] = x;
+    if (deg > 0) {
+        if (!CHECK || dpos < room) {
+            col[dpos] = int32_t(vv);
+            val[dpos] = dsum;
         }
-        zeros += x == 0.0 ? 1 : 0;
-        ++o;
-    };
-    unsigned prev = 0xffffffffu;
+        zeros += dsum == 0.0 ? 1 : 0;
+    }
     double sum = 0.0;
-    bool diag = false;
+    int r = 0;  // runs written so far
 #pragma unroll
-    for (int j = 0; j <= 2 * MAXD; ++j) {
-        const unsigned key = j < 2 * MAXD ? sk[j] : 0xffffffffu;
-        const unsigned c = key == 0xffffffffu ? 0xffffffffu : (key >> 4);
-        if (c != prev) {
-            if (prev != 0xffffffffu) emit(prev, sum);
-            if (!diag && vv < c) {
-                emit(vv, dsum);
-                diag = true;
+    for (int j = 0; j < 2 * MAXD; ++j) {
+        const unsigned key = sk[j];
+        const unsigned nxt = j + 1 < 2 * MAXD ? sk[j + 1] : 0xffffffffu;
+        if (key != 0xffffffffu) {
+            const bool st = j == 0 || ((key ^ sk[j - 1]) >> 4) != 0;
+            sum = FADD(st ? 0.0 : sum, v12[key & 15]);
+            if (((key ^ nxt) >> 4) != 0) {  // run ends: its column and sum
+                const unsigned c = key >> 4;
+                const int idx = r + (c > vv ? 1 : 0);
+                if (!CHECK || idx < room) {
+                    col[idx] = int32_t(c);
+                    val[idx] = sum;
+                }
+                zeros += sum == 0.0 ? 1 : 0;
+                ++r;
             }
-            sum = 0.0;
-            prev = c;
-        }
-        if (j < 2 * MAXD && c != 0xffffffffu) {
-            const int sl = int(key & 15);
-            sum = FADD(sum, R.vals[(1 + (sl & 1)) * CAP + start + (sl >> 1)]);
         }
     }
     return zeros;
@@ -1155,14 +1156,15 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     //    slow gathers of another bucket
     int64_t count = 0, excl = 0, total = 0;
     unsigned sk[NC];
+    int dpos = 0;  // scalar fast rows: columns left of the diagonal
     if (EARLY && fast) {
         row_keys(R, start, deg, sk);
-        unsigned prev = 0xffffffffu, distinct = 0;
+        unsigned distinct = 0;
 #pragma unroll
-        for (int j = 0; j < NC; ++j) {
-            const unsigned c = sk[j] == 0xffffffffu ? 0xffffffffu : (sk[j] >> 4);
-            if (c != 0xffffffffu && c != prev) ++distinct;
-            prev = c;
+        for (int j = 0; j < NC; ++j) {  // run starts among the valid keys; those below the diagonal
+            const bool st = sk[j] != 0xffffffffu && (j == 0 || ((sk[j] ^ sk[j - 1]) >> 4) != 0);
+            distinct += st ? 1u : 0u;
+            dpos += (st && (sk[j] >> 4) < vv) ? 1 : 0;
         }
         count = deg == 0 ? 0 : int64_t(NV) * (distinct + 1);  // no triplet, no entry (isolated vertex)
     }
@@ -1196,8 +1198,13 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
                 const int vl = s_own[i];
                 double rv[RVALS];
                 incidence_values<KIND>(A, ka[u] >> 2, int(ka[u] & 3u), g[u], s_oq[vl], s_ow[vl], rv);
+                if constexpr (KIND == FA_KIND_ELASTIC) {
 #pragma unroll
-                for (int j = 0; j < RVALS; ++j) R.vals[j * CAP + i] = rv[j];
+                    for (int j = 0; j < RVALS; ++j) R.vals[j * CAP + i] = rv[j];
+                } else {  // own column, then the two neighbour columns side by side (one 16-byte store)
+                    R.vals[i] = rv[0];
+                    *reinterpret_cast<double2*>(R.vals + CAP + 2 * i) = make_double2(rv[1], rv[2]);
+                }
             }
         }
     }
@@ -1215,7 +1222,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         const bool staged = !__syncthreads_or(slow) && total <= CAP;
         double* sv = reinterpret_cast<double*>(R.n1);    // [CAP], spans n1 and n2
         int32_t* sc = reinterpret_cast<int32_t*>(R.ka);  // [CAP]
-        if (staged && fast) zeros = walk_row<KIND, false>(R, sk, start, deg, vv, sc + excl, sv + excl, 0);
+        if (staged && fast) zeros = walk_row<KIND, false>(R, sk, start, deg, vv, dpos, sc + excl, sv + excl, 0);
         TL(b, 3);
         base = lookback_wait(A.status, b, uint64_t(total), &s_prefix);  // ends with a barrier
         TL(b, 4);
@@ -1237,7 +1244,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
             }
         } else {
             const int64_t o = int64_t(base) + excl;
-            if (fast) zeros = walk_row<KIND, true>(R, sk, start, deg, vv, A.col + o, A.val + o, A.capacity - o);
+            if (fast) zeros = walk_row<KIND, true>(R, sk, start, deg, vv, dpos, A.col + o, A.val + o, A.capacity - o);
             if (slow)
                 zeros = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc],
                                           s_ow[vloc], s, o, true, true, true)
