@@ -119,9 +119,8 @@ int fa_assemble(fa_plan* plan, int kind, const double* d_q, const double* d_area
 
 /* Cold OptV2 in one call: fa_plan_build(d_me) followed by fa_assemble, i.e. the whole
  * reference assemble(mesh, kind, OPTV2) (assembly.py:419-452) on device buffers.  Plan
- * build errors land in d_build_result, numeric ones in d_result.  For MASSW the
- * per-triangle weight records (which need no plan) are computed concurrently with the plan
- * build on a library-owned low-priority stream; everything joins back into `stream`.
+ * build errors land in d_build_result, numeric ones in d_result.  For MASSW the plan's
+ * connectivity pass also computes the per-triangle weight records (no separate pass).
  * capacity: >= fa_plan_capacity after the build; 3 * (2 * 3 * nme + rows) (x4 for ELASTIC's
  * 2x2 blocks: use fa_plan_capacity's formula with 3 * nme incidences) is always enough. */
 int fa_assemble_cold(fa_plan* plan, const int32_t* d_me, int kind, const double* d_q,

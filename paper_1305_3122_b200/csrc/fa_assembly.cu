@@ -162,10 +162,56 @@ struct PlanArgs {
     // ({k, c0, c1, c2} at block * chunk ..), so K3 skips the others
     uint4* tri;             // null for the whole mesh
     unsigned* tri_cnt;      // per K1/K3 block
+    // weighted mass (fa_assemble_cold): K1 also writes the triangles' W records (k_tri_wt's
+    // work, from the connectivity it reads anyway); null otherwise
+    const double* wt_areas;
+    const double* wt_w;
+    double4* Wt;
 };
 
 __device__ __forceinline__ bool tri_ids_valid(int c0, int c1, int c2, int64_t nq) {
     return unsigned(c0) < nq && unsigned(c1) < nq && unsigned(c2) < nq;
+}
+
+__device__ __forceinline__ void tri_wt_store(double4* Wt, int64_t k, double ar, const double (&wc)[3], uint64_t keep);
+
+// K1's W records for triangles [k0, k1) (weighted mass, cold path): k_tri_wt's work on this
+// block's chunk, the connectivity reread from L2 right after the histogram pass
+__device__ __noinline__ void hist_tri_wt(const PlanArgs& P, int64_t k0, int64_t k1) {
+    const uint64_t pol = l2_evict_first_policy();
+    const uint64_t keep = l2_evict_last_policy();
+#ifndef FA_HIST_WT_U
+#define FA_HIST_WT_U 2
+#endif
+    constexpr int U = FA_HIST_WT_U;  // triangles in flight per thread
+    for (int64_t k0u = k0 + threadIdx.x; k0u < k1; k0u += U * PLACE_THREADS) {
+        int c[U][3];
+        double ar[U], wc[U][3];
+        bool own[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t k = k0u + u * PLACE_THREADS;
+            c[u][0] = c[u][1] = c[u][2] = -1;
+            if (k < k1) {
+                load_tri_ids(P.me, k, c[u][0], c[u][1], c[u][2]);
+                ar[u] = ld_stream_f64(P.wt_areas + k, pol);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            bool any = false;
+#pragma unroll
+            for (int a = 0; a < 3; ++a) any |= c[u][a] >= P.v0 && c[u][a] < P.v1;
+            own[u] = k0u + u * PLACE_THREADS < k1 && any;
+            if (own[u])
+#pragma unroll
+                for (int a = 0; a < 3; ++a)  // out-of-range ids (reported by the histogram) read nothing
+                    wc[u][a] = unsigned(c[u][a]) < P.nq ? ld_keep_f64(P.wt_w + c[u][a], keep) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+            if (own[u]) tri_wt_store(P.Wt, k0u + u * PLACE_THREADS, ar[u], wc[u], keep);
+    }
 }
 
 // K1: owned incidences per (block, part) and per part; index validation (sparse.py:131-137 semantics: first bad
@@ -218,6 +264,7 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
         }
     }
     __syncthreads();
+    if (P.Wt) hist_tri_wt(P, k0, k1);
     if (P.tri && threadIdx.x == 0) P.tri_cnt[blockIdx.x] = s_tn;
     unsigned* row = P.M + int64_t(blockIdx.x) * P.nparts;
     if (!P.fine_hist) {
@@ -1578,6 +1625,19 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const unsigned long lon
 
 // Weighted mass: W_c = (w[me[k,c]] * area_k) / 30 for the three corners, once per triangle
 // (assembly.py:232-234), coalesced; the row kernel gathers one 32-byte record per incidence.
+// W_c = (w[me[k, c]] * area_k) / 30 for the three corners (assembly.py:232-234), stored as one
+// 32-byte record with an L2 evict-last priority (the row kernel gathers it per incidence)
+__device__ __forceinline__ void tri_wt_store(double4* Wt, int64_t k, double ar, const double (&wc)[3], uint64_t keep) {
+    double4 r;
+    r.x = ddiv_rcp(FMUL(wc[0], ar), 30.0, FA_RCP30);
+    r.y = ddiv_rcp(FMUL(wc[1], ar), 30.0, FA_RCP30);
+    r.z = ddiv_rcp(FMUL(wc[2], ar), 30.0, FA_RCP30);
+    r.w = 0.0;
+    asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(Wt + k), "d"(r.x), "d"(r.y),
+                 "d"(r.z), "d"(r.w), "l"(keep)
+                 : "memory");
+}
+
 #ifndef FA_TRI_WT_U
 #define FA_TRI_WT_U 4
 #endif
@@ -1616,19 +1676,8 @@ __global__ void __launch_bounds__(256) k_tri_wt(const int32_t* __restrict__ me, 
             for (int a = 0; a < 3; ++a)  // out-of-range ids (reported by the plan build) read nothing
                 wc[u][a] = unsigned(c[u][a]) < nq ? ld_keep_f64(w + c[u][a], keep) : 0.0;
 #pragma unroll
-    for (int u = 0; u < TRI_WT_U; ++u) {
-        const int64_t k = k0 + u * 256;
-        if (own[u]) {
-            double4 r;
-            r.x = ddiv_rcp(FMUL(wc[u][0], ar[u]), 30.0, FA_RCP30);
-            r.y = ddiv_rcp(FMUL(wc[u][1], ar[u]), 30.0, FA_RCP30);
-            r.z = ddiv_rcp(FMUL(wc[u][2], ar[u]), 30.0, FA_RCP30);
-            r.w = 0.0;
-            asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(Wt + k), "d"(r.x),
-                         "d"(r.y), "d"(r.z), "d"(r.w), "l"(keep)
-                         : "memory");
-        }
-    }
+    for (int u = 0; u < TRI_WT_U; ++u)
+        if (own[u]) tri_wt_store(Wt, k0 + u * 256, ar[u], wc[u], keep);
 }
 
 // Optional CUDA events recorded around the row kernel (bench.py's per-kernel roofline).  Inside
@@ -1692,9 +1741,7 @@ struct fa_plan {
     unsigned* read_done;      // nb (k_compact)
     int64_t ninc;             // -1 until read back
     bool built;
-    // fa_assemble_cold: W records computed on a low-priority side stream during the plan build
-    cudaStream_t s_hi, s_lo;  // created on first use
-    cudaEvent_t ev_fork, ev_wt, ev_done;
+    // fa_assemble_cold: W records written by the plan's histogram pass, consumed once
     const void* wt_key[3];    // (me, areas, w) the prepared W records belong to; consumed once
     bool wt_ready;
 };
@@ -1702,11 +1749,6 @@ struct fa_plan {
 using namespace fa;
 
 static void plan_free(fa_plan* p) {
-    if (p->s_hi) cudaStreamDestroy(p->s_hi);
-    if (p->s_lo) cudaStreamDestroy(p->s_lo);
-    if (p->ev_fork) cudaEventDestroy(p->ev_fork);
-    if (p->ev_wt) cudaEventDestroy(p->ev_wt);
-    if (p->ev_done) cudaEventDestroy(p->ev_done);
     cudaFree(p->part_off); cudaFree(p->part_fill); cudaFree(p->fine_fill); cudaFree(p->tri); cudaFree(p->tri_cnt); cudaFree(p->M); cudaFree(p->rec); cudaFree(p->skey); cudaFree(p->sn1);
     cudaFree(p->sn2); cudaFree(p->ivptr); cudaFree(p->status);
     cudaFree(p->bsym); cudaFree(p->blen); cudaFree(p->bdrop); cudaFree(p->bshift); cudaFree(p->read_done);
@@ -1820,16 +1862,17 @@ extern "C" int fa_plan_destroy(fa_plan* p) {
     return FA_OK;
 }
 
-// pdl: the plan kernels are launched as programmatic dependents of each other (see
-// launch_pdl); fa_assemble_cold turns it off while the W records run on a side stream, whose
-// blocks fill the SMs the plan kernels' tails leave idle.
-static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* stream, bool pdl);
+// pdl: the plan kernels are launched as programmatic dependents of each other (launch_pdl).
+// wt_areas, wt_w (weighted mass, fa_assemble_cold): K1 also writes the W records.
+static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* stream, bool pdl,
+                      const double* wt_areas = nullptr, const double* wt_w = nullptr);
 
 extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* stream) {
     return plan_build(p, d_me, d_res, stream, true);
 }
 
-static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* stream, bool pdl) {
+static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* stream, bool pdl,
+                      const double* wt_areas, const double* wt_w) {
     if (!p || !d_me || !d_res) { set_error("fa_plan_build: NULL argument"); return FA_ERR_ARGUMENT; }
     cudaStream_t st = as_stream(stream);
     p->ninc = -1;
@@ -1855,6 +1898,11 @@ static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* s
     P.fine_global = p->fine_global;
     P.tri = p->tri; P.tri_cnt = p->tri_cnt;
     P.part_off_f = p->part_off; P.fine_fill = p->fine_fill;
+    P.wt_areas = wt_areas; P.wt_w = wt_w; P.Wt = nullptr;
+    if (wt_areas && wt_w) {
+        if (!p->Wt) FA_CUDA(cudaMalloc(&p->Wt, sizeof(double4) * size_t(p->nme)));
+        P.Wt = p->Wt;
+    }
     const size_t hist_smem = sizeof(unsigned) * (P.fine_hist && !P.fine_global ? p->nparts : p->nparts_c);
     FA_CUDA(cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_smem)));
     FA_CUDA(launch_pdl(pdl ? 1 : -1, k_part_hist, dim3(p->nblk_place), dim3(PLACE_THREADS), hist_smem, st, P));
@@ -1988,45 +2036,21 @@ extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double
     return FA_OK;
 }
 
-// Plan build + numeric assembly in one call (the cold OptV2 of the reference API).  The plan
-// kernels and the row kernel run on a high-priority internal stream; for the weighted mass the
-// W records (which need no plan) are computed on a low-priority one at the same time, filling
-// the SM resources the plan kernels leave idle.  Both join back into `stream`.
+// Plan build + numeric assembly in one call (the cold OptV2 of the reference API).  For the
+// weighted mass the plan's histogram pass (which reads the connectivity anyway) also writes
+// the per-triangle W records, so no separate k_tri_wt pass runs.
 extern "C" int fa_assemble_cold(fa_plan* p, const int32_t* d_me, int kind, const double* d_q, const double* d_areas,
                                 const double* d_w, double lam, double mu, int64_t* d_rowptr, int32_t* d_col,
                                 double* d_val, int64_t capacity, fa_result* d_build_result, fa_result* d_result,
                                 void* stream) {
     if (!p || !d_me || !d_build_result) { set_error("fa_assemble_cold: NULL argument"); return FA_ERR_ARGUMENT; }
-    cudaStream_t st = as_stream(stream);
-    const bool side = kind == FA_KIND_MASSW && d_areas && d_w && p->nb > 0;
-    if (!side) {
-        int rc = fa_plan_build(p, d_me, d_build_result, stream);
-        if (rc != FA_OK) return rc;
-        return fa_assemble(p, kind, d_q, d_areas, d_w, lam, mu, d_rowptr, d_col, d_val, capacity, d_result, stream);
+    // weighted mass: the plan's histogram pass also writes the W records (k_tri_wt's work)
+    const bool wt = kind == FA_KIND_MASSW && d_areas && d_w && p->nb > 0;
+    int rc = plan_build(p, d_me, d_build_result, stream, true, wt ? d_areas : nullptr, wt ? d_w : nullptr);
+    if (rc != FA_OK) return rc;
+    if (wt) {
+        p->wt_key[0] = d_me; p->wt_key[1] = d_areas; p->wt_key[2] = d_w;
+        p->wt_ready = true;
     }
-    if (!p->s_hi) {
-        int lo = 0, hi = 0;
-        FA_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        FA_CUDA(cudaStreamCreateWithPriority(&p->s_hi, cudaStreamNonBlocking, hi));
-        FA_CUDA(cudaStreamCreateWithPriority(&p->s_lo, cudaStreamNonBlocking, lo));
-        FA_CUDA(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming));
-        FA_CUDA(cudaEventCreateWithFlags(&p->ev_wt, cudaEventDisableTiming));
-        FA_CUDA(cudaEventCreateWithFlags(&p->ev_done, cudaEventDisableTiming));
-    }
-    FA_CUDA(cudaEventRecord(p->ev_fork, st));
-    FA_CUDA(cudaStreamWaitEvent(p->s_hi, p->ev_fork, 0));
-    FA_CUDA(cudaStreamWaitEvent(p->s_lo, p->ev_fork, 0));
-    int rc = plan_build(p, d_me, d_build_result, p->s_hi, false);
-    if (rc != FA_OK) return rc;
-    rc = launch_tri_wt(p, d_areas, d_w, p->s_lo);
-    if (rc != FA_OK) return rc;
-    FA_CUDA(cudaEventRecord(p->ev_wt, p->s_lo));
-    FA_CUDA(cudaStreamWaitEvent(p->s_hi, p->ev_wt, 0));
-    p->wt_key[0] = d_me; p->wt_key[1] = d_areas; p->wt_key[2] = d_w;
-    p->wt_ready = true;
-    rc = fa_assemble(p, kind, d_q, d_areas, d_w, lam, mu, d_rowptr, d_col, d_val, capacity, d_result, p->s_hi);
-    if (rc != FA_OK) return rc;
-    FA_CUDA(cudaEventRecord(p->ev_done, p->s_hi));
-    FA_CUDA(cudaStreamWaitEvent(st, p->ev_done, 0));
-    return FA_OK;
+    return fa_assemble(p, kind, d_q, d_areas, d_w, lam, mu, d_rowptr, d_col, d_val, capacity, d_result, stream);
 }
