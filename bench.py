@@ -38,11 +38,15 @@ import numpy as np  # noqa: E402
 
 METRIC = "triangles assembled/sec (device-timed, incl. CSR build)"
 UNIT = "triangles/s"
-def launches_per_step(kind):
-    """Our kernels launched per cold step (fa_assemble_cold); memsets are not counted."""
-    return (["k_reset", "k_part_hist", "k_part_scan", "k_part_place", "k_part_sort"]
-            + (["k_tri_wt (weighted-mass W records, side stream during the plan build)"] if kind == "massw" else [])
-            + ["k_reset", "k_rows", "k_compact (exits at once unless a sum was exactly zero)"])
+def launches_per_step(kind, nme, nq, nv):
+    """Our kernels launched per cold step (fa_assemble_cold); memsets are not counted.  The
+    two-level plan rule mirrors fa_plan_create (more than 8192 parts of 1024 rows, or more than
+    160 MB of part records with more than 256 parts) and adds k_part_split."""
+    nparts = -(-nv // 1024)
+    two_level = nparts > 8192 or (48 * nme // max(nq, 1) * nv > (160 << 20) and nparts > 256)
+    hist = "k_part_hist (weighted mass: also the per-triangle W records)" if kind == "massw" else "k_part_hist"
+    return (["k_reset", hist, "k_part_scan", "k_part_place"] + (["k_part_split"] if two_level else [])
+            + ["k_part_sort", "k_reset", "k_rows", "k_compact (exits at once unless a sum was exactly zero)"])
 DEFAULT_CONFIG = "C2"
 DESCR = {
     "C1": "P1 mass, N=256 seeded jittered/permuted unit square",
@@ -331,7 +335,7 @@ def run_ours(args):
 
     def step(cold=True):
         # current stream (the capture stream inside a graph capture)
-        if cold:  # fa_assemble_cold: plan build + numeric pass (weighted mass: W records alongside the build)
+        if cold:  # fa_assemble_cold: plan build + numeric pass (weighted mass: W records in the build)
             plan.assemble_cold_into(me_d, kind, q_use, a_d, w_d, lam, mu, rowptr, col, val, res)
         else:
             plan.assemble_into(kind, q_use, a_d, w_d, lam, mu, rowptr, col, val, res)
@@ -494,8 +498,8 @@ def run_ours(args):
                      "what": "plan reused (vertex-sorted incidences cached): row kernel only"},
             "clocks": clock_info,
             "e2e": e2e,
-            "gpu_launches": len(launches_per_step(kind)) * args.steps,
-            "gpu_launches_detail": "per step: " + ", ".join(launches_per_step(kind)),
+            "gpu_launches": len(launches_per_step(kind, sm.nme, sm.nq, v1 - v0)) * args.steps,
+            "gpu_launches_detail": "per step: " + ", ".join(launches_per_step(kind, sm.nme, sm.nq, v1 - v0)),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
