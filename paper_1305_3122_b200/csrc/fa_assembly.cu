@@ -60,8 +60,11 @@
 #ifndef FA_ROWS_AU
 #define FA_ROWS_AU 4  // incidences in flight per thread in the row kernel phase a
 #endif
+#ifndef FA_ROWS_MINB_W
+#define FA_ROWS_MINB_W 5  // weighted mass: <= 102 registers (no gather reuse, L1 matters less)
+#endif
 #ifndef FA_ROWS_MINB
-#define FA_ROWS_MINB 4  // scalar kinds: <= 128 registers, no local memory
+#define FA_ROWS_MINB 4  // mass, stiffness: <= 128 registers, no local memory
 #endif
 
 namespace fa {
@@ -767,7 +770,8 @@ struct KindTraits {
     // per-record shared data: scalar kinds store the row's three values, elasticity the 2 x 6
     // entries of its two dof rows (own, n1, n2 vertex columns, x and y)
     static constexpr int RVALS = KIND == FA_KIND_ELASTIC ? 12 : 3;
-    static constexpr int MIN_BLOCKS = KIND == FA_KIND_ELASTIC ? FA_ROWS_MINB_E : FA_ROWS_MINB;
+    static constexpr int MIN_BLOCKS =
+        KIND == FA_KIND_ELASTIC ? FA_ROWS_MINB_E : (KIND == FA_KIND_MASSW ? FA_ROWS_MINB_W : FA_ROWS_MINB);
     static constexpr int CAP = KIND == FA_KIND_ELASTIC ? FA_CAPB_E : CAPB;  // incidences in shared memory
     static constexpr size_t REC_BYTES = size_t(CAP) * (RVALS * 8 + 12);
     static constexpr int STAGE = int(REC_BYTES / 12);  // staged entries fitting the records area
@@ -802,7 +806,7 @@ __device__ __forceinline__ Gathered gather_incidence(const RowsArgs& A, unsigned
         g.p2 = ld_keep_f64x2(A.q + n2, pol);
     }
     if (KIND == FA_KIND_MASSW)  // the triangle's three W (k_tri_wt): one 32-byte gather
-        asm volatile("ld.global.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
+        asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.f64 {%0, %1, %2, %3}, [%4], %5;"
                      : "=d"(g.wt.x), "=d"(g.wt.y), "=d"(g.wt.z), "=d"(g.wt.w)
                      : "l"(A.Wt + k), "l"(pol));
     return g;
@@ -1266,6 +1270,11 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         //      into the compact staging.  The staging lies in the plan-entry arrays, dead once
         //      phase a is done (n1 + n2 + ka hold 12 bytes per incidence slot, a staged entry
         //      is 12 bytes), so the records' values stay intact for the unstaged fallback.
+#ifdef FA_ROWS_RESORT
+        // the sorted keys are rebuilt from the plan entries (still intact) instead of being
+        // held in registers across phase a
+        if (fast) row_keys(R, start, deg, sk);
+#endif
         const bool staged = !__syncthreads_or(slow) && total <= CAP;
         double* sv = reinterpret_cast<double*>(R.n1);    // [CAP], spans n1 and n2
         int32_t* sc = reinterpret_cast<int32_t*>(R.ka);  // [CAP]

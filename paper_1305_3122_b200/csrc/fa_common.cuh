@@ -129,9 +129,12 @@ __device__ __forceinline__ void st_stream_i32x4(int* p, int x, int y, int z, int
                  : "memory");
 }
 
-// Randomly gathered arrays (areas, q, w) are pulled into L2 once, sequentially, with an
-// evict-last priority, and gathered with the same priority: every later random access hits L2
-// instead of paying a DRAM round trip per 32-byte sector.
+// Randomly gathered arrays (areas, q, w, W records) are gathered with an L2 evict-last
+// priority, so later random accesses hit L2 instead of paying a DRAM round trip per 32-byte
+// sector.  Per-triangle data (areas, W records) and the weights are gathered without L1
+// allocation: they have no L1 reuse, and allocating their lines thrashes L1 (weighted-mass row
+// kernel -3 %, and it then runs faster with five blocks per SM).  Coordinates do allocate:
+// every neighbour of a row is gathered twice (as n1 of one triangle and n2 of the next).
 __device__ __forceinline__ uint64_t l2_evict_last_policy() {
     uint64_t p;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -139,7 +142,7 @@ __device__ __forceinline__ uint64_t l2_evict_last_policy() {
 }
 __device__ __forceinline__ double ld_keep_f64(const double* p, uint64_t pol) {
     double v;
-    asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
     return v;
 }
 __device__ __forceinline__ double2 ld_keep_f64x2(const double2* p, uint64_t pol) {
