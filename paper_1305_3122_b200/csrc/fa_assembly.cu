@@ -79,6 +79,11 @@ constexpr int BV = FA_BV;          // vertices per row bucket
 #ifndef FA_CAPB
 #define FA_CAPB (8 * BV)
 #endif
+#ifndef FA_CAPB_W
+// weighted mass (five blocks per SM): a smaller bucket leaves L1 more room; the mean degree of
+// a planar triangulation is below 6, so overflowing buckets (general path) stay rare
+#define FA_CAPB_W (7 * BV)
+#endif
 constexpr int CAPB = FA_CAPB;      // incidences per bucket held in shared memory
 constexpr int MAXD = 8;            // incidences per row on the register fast path
 constexpr int PLOG0 = 10;          // log2 of the minimum part size (vertices)
@@ -612,7 +617,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_cons
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const unsigned i = i0 + u * SORT_THREADS;
-                y[u] = i < n ? ry[4 * size_t(i)] : 0xffffffffu;
+                y[u] = i < n ? ry[4 * size_t(i)] : 0xffffffffu;  // L1-allocating: the record pass below hits
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u)
@@ -772,7 +777,8 @@ struct KindTraits {
     static constexpr int RVALS = KIND == FA_KIND_ELASTIC ? 12 : 3;
     static constexpr int MIN_BLOCKS =
         KIND == FA_KIND_ELASTIC ? FA_ROWS_MINB_E : (KIND == FA_KIND_MASSW ? FA_ROWS_MINB_W : FA_ROWS_MINB);
-    static constexpr int CAP = KIND == FA_KIND_ELASTIC ? FA_CAPB_E : CAPB;  // incidences in shared memory
+    static constexpr int CAP =  // incidences in shared memory
+        KIND == FA_KIND_ELASTIC ? FA_CAPB_E : (KIND == FA_KIND_MASSW ? FA_CAPB_W : CAPB);
     static constexpr size_t REC_BYTES = size_t(CAP) * (RVALS * 8 + 12);
     static constexpr int STAGE = int(REC_BYTES / 12);  // staged entries fitting the records area
 };
