@@ -802,6 +802,7 @@ __device__ __forceinline__ Gathered gather_incidence(const RowsArgs& A, unsigned
 #ifdef FA_EXP_NOGATHER
     g.p1 = make_double2(double(n1), 1.0); g.p2 = make_double2(double(n2), 2.0);
     g.w1 = double(n1 + 1); g.w2 = double(n2 + 1); g.ar = double(k + 1) * 1e-6;
+    g.wt = make_double4(double(k + 1), double(k + 2), double(k + 3), 0.0);
     return g;
 #endif
     g.p1 = g.p2 = make_double2(0.0, 0.0);
