@@ -60,6 +60,9 @@
 #ifndef FA_ROWS_AU
 #define FA_ROWS_AU 4  // incidences in flight per thread in the row kernel phase a
 #endif
+#ifndef FA_ROWS_AU_W
+#define FA_ROWS_AU_W 3  // weighted mass: W records in flight per thread (no spills at 96 registers)
+#endif
 #ifndef FA_ROWS_MINB_W
 #define FA_ROWS_MINB_W 5  // weighted mass: <= 102 registers (no gather reuse, L1 matters less)
 #endif
@@ -1239,7 +1242,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     // ---- a) per incidence (balanced over threads): gathers from the L2-resident arrays, the
     //         row of the element matrix -> shared memory
     {
-        constexpr int AU = KIND == FA_KIND_ELASTIC ? FA_ROWS_AU_E : FA_ROWS_AU;
+        constexpr int AU = KIND == FA_KIND_ELASTIC ? FA_ROWS_AU_E : (KIND == FA_KIND_MASSW ? FA_ROWS_AU_W : FA_ROWS_AU);
         for (int i0 = tid; i0 < n; i0 += NT * AU) {
             unsigned ka[AU];
             Gathered g[AU];
