@@ -315,6 +315,11 @@ def run_ours(args):
     a_d = torch.from_numpy(areas).to(dev)
     w_d = torch.from_numpy(sm.weights).to(dev) if kind == "massw" else None
     q_use = q_d if kind in ("stiff", "elastic") else None
+    # as assemble() does for a Mesh whose areas it computed: stiffness and elasticity recompute
+    # them from the coordinates they gather anyway (bitwise compute_areas,
+    # test_recomputed_areas_are_bitwise) instead of gathering one more array per incidence
+    if kind in ("stiff", "elastic"):
+        a_d = None
     v0, v1 = row_blocks(sm.nq, world)[rank]
     plan = fa.AssemblyPlan(sm.nme, sm.nq, v0, v1)
     plan.build(me_d)
@@ -427,9 +432,10 @@ def run_ours(args):
     # end to end through the host-buffer API: pinned inputs -> device, plan, assemble, CSR -> host
     e2e = None
     if args.e2e_steps > 0:
-        ha = HostAssembler(kind, sm.nq, sm.nme, v0, v1, depth=2)
+        recompute = kind in ("stiff", "elastic")  # areas from q on the device, as above
+        ha = HostAssembler(kind, sm.nq, sm.nme, v0, v1, recompute_areas=recompute, depth=2)
         pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()  # noqa: E731
-        h_me, h_q, h_a = pin(me32), pin(sm.vertices), pin(areas)
+        h_me, h_q, h_a = pin(me32), pin(sm.vertices), (None if recompute else pin(areas))
         h_w = pin(sm.weights) if kind == "massw" else None
         h_q = h_q if kind in ("stiff", "elastic") else None
         lat = []

@@ -19,6 +19,8 @@ dev = torch.device("cuda")
 me = torch.from_numpy(sm.connectivity.astype(np.int32)).to(dev)
 q = torch.from_numpy(sm.vertices).to(dev)
 a = torch.from_numpy(fa.compute_areas(sm.vertices, sm.connectivity)).to(dev)
+if kind in ("stiff", "elastic"):  # recomputed from q, as assemble() does for an exact-area Mesh
+    a = None
 w = torch.from_numpy(sm.weights).to(dev) if kind == "massw" else None
 sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 from paper_1305_3122_b200.dist import row_blocks  # noqa: E402
