@@ -58,7 +58,9 @@ typedef struct fa_result {
     int64_t col_error_pos;     /* first out-of-range column index position (triplets)      */
     int64_t dropped;           /* positions dropped because their sum was exactly 0.0     */
     int64_t heavy_rows;        /* rows that took the general (degree > 8) path             */
-    int64_t reserved[2];       /* internal: [0] exact zeros left for the in-place compaction */
+    int64_t reserved[1];       /* internal: exact zeros left for the in-place compaction    */
+    int64_t repeat_error_pos;  /* first connectivity position repeating a vertex id of its
+                                  triangle (femasm Mesh rejects those, mesh.py:98-103)       */
 } fa_result;
 
 /* Map a HOST copy of an fa_result block to a status code (FA_OK when clean). */

@@ -62,11 +62,23 @@ class FaResult(ctypes.Structure):
         ("col_error_pos", ctypes.c_int64),
         ("dropped", ctypes.c_int64),
         ("heavy_rows", ctypes.c_int64),
-        ("reserved", ctypes.c_int64 * 2),
+        ("reserved", ctypes.c_int64 * 1),
+        ("repeat_error_pos", ctypes.c_int64),
     ]
 
 
 RESULT_WORDS = ctypes.sizeof(FaResult) // 8
+
+
+def result_from_words(words) -> FaResult:
+    """An FaResult from the block's RESULT_WORDS int64 words (a host copy of the device block)."""
+    r = FaResult()
+    off = 0
+    for name, typ in FaResult._fields_:
+        if not issubclass(typ, ctypes.Array):
+            setattr(r, name, int(words[off]))
+        off += ctypes.sizeof(typ) // 8
+    return r
 
 _P = ctypes.c_void_p
 _I64 = ctypes.c_int64

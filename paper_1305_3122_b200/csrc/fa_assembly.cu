@@ -123,7 +123,7 @@ __global__ void k_reset(fa_result* r, unsigned* z32, int64_t n32, uint64_t* z64,
         r->dropped = 0;
         r->heavy_rows = 0;
         r->reserved[0] = 0;
-        r->reserved[1] = 0;
+        r->repeat_error_pos = INT64_MAX;
     }
 }
 
@@ -136,7 +136,7 @@ __global__ void k_reset_result(fa_result* r) {
         r->dropped = 0;
         r->heavy_rows = 0;
         r->reserved[0] = 0;
-        r->reserved[1] = 0;
+        r->repeat_error_pos = INT64_MAX;
     }
 }
 
@@ -180,8 +180,9 @@ struct PlanArgs {
     double4* Wt;
 };
 
+// a triangle takes part only with three in-range, pairwise distinct vertex ids
 __device__ __forceinline__ bool tri_ids_valid(int c0, int c1, int c2, int64_t nq) {
-    return unsigned(c0) < nq && unsigned(c1) < nq && unsigned(c2) < nq;
+    return unsigned(c0) < nq && unsigned(c1) < nq && unsigned(c2) < nq && c0 != c1 && c1 != c2 && c0 != c2;
 }
 
 __device__ __forceinline__ void tri_wt_store(double4* Wt, int64_t k, double ar, const double (&wc)[3], uint64_t keep);
@@ -263,6 +264,9 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
                     P.tri[k0 + atomicAdd(&s_tn, 1u)] =
                         make_uint4(unsigned(k), unsigned(c[u][0]), unsigned(c[u][1]), unsigned(c[u][2]));
             }
+#pragma unroll
+            if (c[u][0] == c[u][1] || c[u][1] == c[u][2] || c[u][0] == c[u][2])  // first repeating corner
+                atomic_min_i64(&P.res->repeat_error_pos, 3 * k + (c[u][0] == c[u][1] ? 1 : 2));
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 const int64_t v = c[u][a];

@@ -20,7 +20,7 @@ __global__ void k_reset_result_b(fa_result* r) {
         r->dropped = 0;
         r->heavy_rows = 0;
         r->reserved[0] = 0;
-        r->reserved[1] = 0;
+        r->repeat_error_pos = INT64_MAX;
     }
 }
 

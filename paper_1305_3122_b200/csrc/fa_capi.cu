@@ -36,7 +36,8 @@ extern "C" const char* fa_version(void) { return "femasm_b200 0.1.0 sm_100a"; }
 
 extern "C" int fa_result_status(const fa_result* r) {
     if (!r) return FA_ERR_ARGUMENT;
-    if (r->index_error_pos != INT64_MAX || r->col_error_pos != INT64_MAX) return FA_ERR_INDEX;
+    if (r->index_error_pos != INT64_MAX || r->col_error_pos != INT64_MAX || r->repeat_error_pos != INT64_MAX)
+        return FA_ERR_INDEX;
     if (r->degenerate_index != INT64_MAX) return FA_ERR_DEGENERATE;
     return FA_OK;
 }

@@ -39,11 +39,7 @@ class ResultBlock:
         return self.dev.data_ptr()
 
     def fetch(self) -> _lib.FaResult:
-        host = self.dev.cpu().numpy()
-        r = _lib.FaResult()
-        for i, (name, _) in enumerate(_lib.FaResult._fields_[:6]):
-            setattr(r, name, int(host[i]))
-        return r
+        return _lib.result_from_words(self.dev.cpu().numpy())
 
 
 def to_device(arr: np.ndarray, dtype=None):

@@ -163,10 +163,8 @@ class HostAssembler:
         if s.ticket != ticket:
             raise ValueError(f"step {ticket} is not in flight (slot holds {s.ticket})")
         s.ev_meta.synchronize()
-        r, rb = _lib.FaResult(), _lib.FaResult()
-        for i, (name, _) in enumerate(_lib.FaResult._fields_[:6]):
-            setattr(r, name, int(s.h_res[i]))
-            setattr(rb, name, int(s.h_res[_lib.RESULT_WORDS + i]))
+        r = _lib.result_from_words(s.h_res[: _lib.RESULT_WORDS])
+        rb = _lib.result_from_words(s.h_res[_lib.RESULT_WORDS:])
         self.last_result, self.last_build_result = r, rb
         nnz = int(r.nnz)
         if nnz > self._cap:  # the capacity is sized once, from the first step's plan
@@ -197,6 +195,8 @@ def _host_assemble(kind, nq, nme, me, q=None, areas=None, w=None, lam=0.0, mu=0.
     r = a.last_result
     if a.last_build_result.index_error_pos != _lib.INT64_MAX:
         raise ValueError("connectivity index out of range [0, nq)")
+    if a.last_build_result.repeat_error_pos != _lib.INT64_MAX:
+        raise ValueError("triangle with repeated vertex indices")
     if r.degenerate_index != _lib.INT64_MAX:
         from .mesh import DegenerateTriangleError
 

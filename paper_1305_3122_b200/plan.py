@@ -47,6 +47,8 @@ class AssemblyPlan:
         r = self._build_res.fetch()
         if r.index_error_pos != _lib.INT64_MAX:
             raise ValueError("connectivity index out of range [0, nq)")
+        if r.repeat_error_pos != _lib.INT64_MAX:
+            raise ValueError("triangle with repeated vertex indices")
 
     def rows(self, kind: str) -> int:
         return (self.row_end - self.row_begin) * KIND_ROWS_PER_VERTEX[kind]

@@ -34,12 +34,23 @@ def test_version_and_result_status_without_gpu():
     r.index_error_pos = _lib.INT64_MAX
     r.col_error_pos = _lib.INT64_MAX
     r.degenerate_index = _lib.INT64_MAX
+    r.repeat_error_pos = _lib.INT64_MAX
     assert lib.fa_result_status(ctypes.addressof(r)) == _lib.FA_OK
+    r.repeat_error_pos = 5
+    assert lib.fa_result_status(ctypes.addressof(r)) == _lib.FA_ERR_INDEX
+    r.repeat_error_pos = _lib.INT64_MAX
     r.degenerate_index = 3
     assert lib.fa_result_status(ctypes.addressof(r)) == _lib.FA_ERR_DEGENERATE
     r.index_error_pos = 0
     assert lib.fa_result_status(ctypes.addressof(r)) == _lib.FA_ERR_INDEX
     assert ctypes.sizeof(_lib.FaResult) == 64
+
+
+def test_result_words_map_to_fields():
+    words = list(range(10, 10 + _lib.RESULT_WORDS))
+    r = _lib.result_from_words(words)
+    assert (r.nnz, r.degenerate_index, r.index_error_pos, r.col_error_pos) == (10, 11, 12, 13)
+    assert (r.dropped, r.heavy_rows, r.repeat_error_pos) == (14, 15, 17)
 
 
 def test_plan_argument_errors_are_reported_before_touching_the_device():

@@ -6,6 +6,7 @@ import numpy as np
 import pytest
 
 import paper_1305_3122_b200 as fa
+from paper_1305_3122_b200 import _lib
 from helpers import assert_same_csc, csc_digests
 from oracle import c_oracle
 from oracle import femasm_oracle as fo
@@ -178,6 +179,20 @@ def test_connectivity_out_of_range_is_reported():
     plan.build(torch.from_numpy(C).cuda())
     with pytest.raises(ValueError, match="out of range"):
         plan.check_build()
+
+
+def test_repeated_vertex_is_reported():
+    """femasm's Mesh rejects a triangle that repeats a vertex id (mesh.py:98-103); a caller of
+    the C ABI that skips Mesh gets the plan build's error, and the triangle is left out."""
+    import torch
+
+    C = np.array([[0, 1, 2], [1, 3, 3], [2, 2, 0]], dtype=np.int32)
+    plan = fa.AssemblyPlan(3, 4)
+    plan.build(torch.from_numpy(C).cuda())
+    with pytest.raises(ValueError, match="repeated vertex"):
+        plan.check_build()
+    r = plan._build_res.fetch()
+    assert r.repeat_error_pos == 3 * 1 + 2 and r.index_error_pos == _lib.INT64_MAX
 
 
 def _structured_square(n):
