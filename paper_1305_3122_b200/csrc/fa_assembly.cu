@@ -58,7 +58,7 @@
 #define FA_ROWS_AU_E 1  // elasticity (12 values per incidence)
 #endif
 #ifndef FA_ROWS_AU
-#define FA_ROWS_AU 4  // incidences in flight per thread in the row kernel phase a
+#define FA_ROWS_AU 3  // mass, stiffness: incidences in flight per thread in the row kernel phase a
 #endif
 #ifndef FA_ROWS_AU_W
 #define FA_ROWS_AU_W 3  // weighted mass: W records in flight per thread (no spills at 96 registers)
