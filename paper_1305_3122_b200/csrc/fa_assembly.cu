@@ -1152,6 +1152,8 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     __shared__ uint64_t s_prefix;
     __shared__ int64_t s_warp[NT / 32];
     __shared__ int64_t s_total;
+    __shared__ unsigned s_zeros;
+    if (threadIdx.x == 0) s_zeros = 0;  // ordered before its atomics by next_tile's barrier
 
     const int tid = threadIdx.x;
     const uint64_t pol_first = l2_evict_first_policy();
@@ -1484,8 +1486,12 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     }
     }  // !EARLY
     // zero sums of the bucket -> compaction data (k_compact runs only when some exist)
-    block_exclusive_scan<NT>(zeros, s_warp, &s_total);
-    const unsigned bz = unsigned(s_total);
+    {  // the bucket's zero count: warp sums, one shared atomic per warp that has any
+        const unsigned wz = __reduce_add_sync(0xffffffffu, unsigned(zeros));
+        if ((tid & 31) == 0 && wz) atomicAdd(&s_zeros, wz);
+    }
+    __syncthreads();
+    const unsigned bz = s_zeros;
     if (tid == 0) {
         A.bsym[b] = base;
         A.blen[b] = unsigned(total);
