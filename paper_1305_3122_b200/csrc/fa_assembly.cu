@@ -1163,7 +1163,29 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     const int64_t nvl = A.v1 - A.v0;
     const int64_t vb0 = b * BV;  // first vertex of the bucket (row-block local)
     const int nvb = int(min(int64_t(BV), nvl - vb0));
+    // the bucket's incidence range first; the mass kinds issue their plan-entry loads together
+    // with the row starts (one DRAM round trip less before the first barrier; stiffness and
+    // elasticity, which also load the own coordinates here, are faster without the extra
+    // registers)
     const unsigned gbase = A.ivptr[vb0];
+    const int ntot = int(A.ivptr[vb0 + nvb] - gbase);
+    const bool overflow = ntot > CAP;
+    const int n = overflow ? 0 : ntot;
+    constexpr int PER = (CAP + NT - 1) / NT;
+    constexpr bool EARLY_LOAD = KIND == FA_KIND_MASS || KIND == FA_KIND_MASSW;
+    unsigned lk[PER], l1[PER], l2[PER];
+    auto load_entries = [&]() {
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+            const int i = tid + u * NT;
+            if (i < n) {
+                lk[u] = ld_stream_u32(A.skey + gbase + i, pol_first);
+                l1[u] = ld_stream_u32(A.sn1 + gbase + i, pol_first);
+                l2[u] = ld_stream_u32(A.sn2 + gbase + i, pol_first);
+            }
+        }
+    };
+    if constexpr (EARLY_LOAD) load_entries();
     for (int i = tid; i <= BV; i += NT) s_vst[i] = int(A.ivptr[vb0 + min(i, nvb)] - gbase);
     const int64_t vbase = A.v0 + vb0;
     // own coordinates: gradients, or the area when none is given (the weighted mass never reads q)
@@ -1174,31 +1196,17 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         s_ow[i] = 0.0;  // (the weighted mass reads its W per triangle, k_tri_wt)
     }
     __syncthreads();
-    const bool overflow = s_vst[BV] > CAP;
-    const int n = overflow ? 0 : s_vst[BV];
     for (int vl = tid; vl < nvb && !overflow; vl += NT)
         for (int j = s_vst[vl]; j < s_vst[vl + 1]; ++j) s_own[j] = (unsigned char)vl;
     // ---- s) the bucket's plan entries -> shared memory (coalesced)
-    {  // all loads of a thread issued before the first store (one DRAM round trip)
-        constexpr int PER = (CAP + NT - 1) / NT;
-        unsigned lk[PER], l1[PER], l2[PER];
+    if constexpr (!EARLY_LOAD) load_entries();
 #pragma unroll
-        for (int u = 0; u < PER; ++u) {
-            const int i = tid + u * NT;
-            if (i < n) {
-                lk[u] = ld_stream_u32(A.skey + gbase + i, pol_first);
-                l1[u] = ld_stream_u32(A.sn1 + gbase + i, pol_first);
-                l2[u] = ld_stream_u32(A.sn2 + gbase + i, pol_first);
-            }
-        }
-#pragma unroll
-        for (int u = 0; u < PER; ++u) {
-            const int i = tid + u * NT;
-            if (i < n) {
-                R.ka[i] = lk[u];
-                R.n1[i] = int(l1[u]);
-                R.n2[i] = int(l2[u]);
-            }
+    for (int u = 0; u < PER; ++u) {
+        const int i = tid + u * NT;
+        if (i < n) {
+            R.ka[i] = lk[u];
+            R.n1[i] = int(l1[u]);
+            R.n2[i] = int(l2[u]);
         }
     }
     __syncthreads();
@@ -1275,7 +1283,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
             }
         }
     }
-    __syncthreads();
+    const bool any_slow = __syncthreads_or(slow);  // also the end of phase a
     TL(b, 2);
 
     int64_t zeros = 0;
@@ -1291,7 +1299,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         // held in registers across phase a
         if (fast) row_keys(R, start, deg, sk);
 #endif
-        const bool staged = !__syncthreads_or(slow) && total <= CAP;
+        const bool staged = !any_slow && total <= CAP;
         double* sv = reinterpret_cast<double*>(R.n1);    // [CAP], spans n1 and n2
         int32_t* sc = reinterpret_cast<int32_t*>(R.ka);  // [CAP]
         if (staged && fast) zeros = walk_row<KIND, false>(R, sk, start, deg, vv, dpos, sc + excl, sv + excl, 0);
