@@ -1247,8 +1247,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         count = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc], s_ow[vloc], s, 0,
                                   false).count;
     if (EARLY) {
-        excl = block_exclusive_scan<NT>(count, s_warp, &s_total);
-        total = s_total;
+        excl = block_exclusive_scan_1b<NT>(count, s_warp, total);
         lookback_publish(A.status, b, uint64_t(total));
     }
     TL(b, 1);
@@ -1395,8 +1394,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
             count = rc.count;
             zeros = rc.zeros;
         }
-        excl = block_exclusive_scan<NT>(count, s_warp, &s_total);
-        total = s_total;
+        excl = block_exclusive_scan_1b<NT>(count, s_warp, total);
         lookback_publish(A.status, b, uint64_t(total));
     }
     TL(b, 3);

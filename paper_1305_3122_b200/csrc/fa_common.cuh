@@ -179,6 +179,28 @@ __device__ __forceinline__ T warp_sum(T v) {
 // Block-wide exclusive scan of one value per thread.  Returns the exclusive prefix of the
 // calling thread; *total receives the block aggregate.  `warp_tot` is shared scratch of
 // BLOCK/32 entries.
+// Same for small blocks (<= 8 warps) with one barrier: every thread adds up the totals of the
+// warps before its own.  `total` receives the block aggregate in every thread.  Consecutive
+// calls on the same `warp_tot` must be separated by a barrier.
+template <int BLOCK, typename T>
+__device__ __forceinline__ T block_exclusive_scan_1b(T v, T* warp_tot, T& total) {
+    constexpr int NW = BLOCK / 32;
+    static_assert(NW <= 8, "small blocks only");
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const T inc = warp_inclusive_scan(v);
+    if (lane == 31) warp_tot[wid] = inc;
+    __syncthreads();
+    T before = T(0), all = T(0);
+#pragma unroll
+    for (int w = 0; w < NW; ++w) {
+        const T t = warp_tot[w];
+        before += w < wid ? t : T(0);
+        all += t;
+    }
+    total = all;
+    return before + inc - v;
+}
+
 template <int BLOCK, typename T>
 __device__ __forceinline__ T block_exclusive_scan(T v, T* warp_tot, T* total) {
     constexpr int NW = BLOCK / 32;
