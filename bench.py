@@ -2,27 +2,38 @@
 """Benchmark of the B200 OptV2 P1 assembly (one JSON line on rank 0).
 
 Metric (BASELINE.json): triangles assembled per second, device-timed, including the CSR
-build, plus achieved HBM GB/s.  Workload: BASELINE configs[1] = C2, the P1 weighted mass
-matrix on the seeded jittered/permuted unit-square mesh with N=1024 (2,097,152 triangles,
-1,050,625 vertices, vertex weights U(0.5, 2)); other configs via --config.
+build, plus achieved HBM GB/s.  Workload (default): BASELINE configs[4] = C5, the P1 stiffness
+matrix on the seeded jittered/permuted unit-square mesh with N=8192 (134,217,728 triangles,
+67,125,249 vertices, ~470 M stored entries) - the largest configuration that fits one GPU.
+C1-C4 via --config (they are parity-test cases, not headline lines).
 
 One step = one complete OptV2 assembly from device-resident inputs: plan build (part
-histogram, staged part placement, per-part vertex sort) + fused row kernel writing
-rowptr/col/val, i.e. the reference's `assemble(mesh, kind, OPTV2)` with nothing cached between
-steps ("cold").  The L2
-is flushed (a 512 MB buffer is zeroed) between timed steps, outside the timed windows.
+histogram, part placement, per-part vertex sort) + fused row kernel writing rowptr/col/val,
+i.e. the reference's `assemble(mesh, kind, OPTV2)` with nothing cached between steps
+("cold").  The L2 is flushed (a 512 MB buffer is zeroed) between timed steps, outside the
+timed windows.  After the timed loop the last step's CSR is hashed and compared with the
+SHA-256 digests of femasm's own output for the same seeded mesh (tests/golden/
+reference_digests.json, produced by running the reference): the line carries the verdict.
 N > 1 (torchrun): rank g assembles the matrix rows of vertex block g (row-block
 decomposition); the step includes the NCCL allgather of the per-rank nnz
 that yields the global row offsets.  The total work is fixed: "scaling": "strong".
 
---impl reference: the reference algorithm on the host CPU (the numpy restatement of femasm's
-OptV2 in oracle/, femasm itself being pure Python/numpy and not shippable), run on all host
-cores as one row-block subset per process.  Rank 0 only.
+CPU legs (test infrastructure never on the measured GPU path):
+  * cpu_baseline (rank 0, N=1): femasm itself (the unmodified reference, installed offline
+    into baseline/_ref; the numpy restatement in oracle/ if that install is missing) on ONE
+    core, timed like femasm bench._time_cell (/root/reference/pkg/src/femasm/bench.py:97-122:
+    one discarded warm-up, median of the timed runs) on a bounded sample: the sub-mesh made of
+    the triangles touching one block of vertex rows (vertices compacted), a few million
+    triangles; femasm OptV2 is linear in nme, so its triangles/s is reported
+    as the full-mesh rate, labelled extrapolated.
+  * --impl reference: the same femasm call on every host core (one row-block sub-mesh per
+    process per step), rank 0 only.
 """
 
 from __future__ import annotations
 
 import argparse
+import hashlib
 import json
 import os
 import statistics
@@ -38,6 +49,18 @@ import numpy as np  # noqa: E402
 
 METRIC = "triangles assembled/sec (device-timed, incl. CSR build)"
 UNIT = "triangles/s"
+DEFAULT_CONFIG = "C5"
+DESCR = {
+    "C1": "P1 mass, N=256 seeded jittered/permuted unit square",
+    "C2": "P1 weighted mass (vertex weights U(0.5,2)), N=1024 seeded jittered/permuted unit square",
+    "C3": "P1 stiffness, N=2048 seeded jittered/permuted unit square",
+    "C4": "2D linear elasticity lam=1 mu=0.5, N=2048 seeded jittered/permuted unit square",
+    "C5": "P1 stiffness, N=8192 seeded jittered/permuted unit square (largest config on one GPU)",
+}
+DIGESTS = REPO / "tests" / "golden" / "reference_digests.json"
+REF_INSTALL = REPO / "baseline" / "_ref"
+
+
 def launches_per_step(kind, nme, nq, nv):
     """Our kernels launched per cold step (fa_assemble_cold); memsets are not counted.  The
     two-level plan rule mirrors fa_plan_create (more than 8192 parts of 1024 rows, or more than
@@ -47,27 +70,22 @@ def launches_per_step(kind, nme, nq, nv):
     hist = "k_part_hist (weighted mass: also the per-triangle W records)" if kind == "massw" else "k_part_hist"
     return (["k_reset", hist, "k_part_scan", "k_part_place"] + (["k_part_split"] if two_level else [])
             + ["k_part_sort", "k_reset", "k_rows", "k_compact (exits at once unless a sum was exactly zero)"])
-DEFAULT_CONFIG = "C2"
-DESCR = {
-    "C1": "P1 mass, N=256 seeded jittered/permuted unit square",
-    "C2": "P1 weighted mass (vertex weights U(0.5,2)), N=1024 seeded jittered/permuted unit square",
-    "C3": "P1 stiffness, N=2048 seeded jittered/permuted unit square",
-    "C4": "2D linear elasticity lam=1 mu=0.5, N=2048 seeded jittered/permuted unit square",
-    "C5": "P1 stiffness, N=8192 seeded jittered/permuted unit square",
-}
 
 
 def parse_args():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=300)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-baseline-runs", type=int, default=2, help="timed runs of the 1-core CPU baseline (0: skip)")
-    ap.add_argument("--e2e-steps", type=int, default=20)
+    ap.add_argument("--e2e-steps", type=int, default=6)
     ap.add_argument("--graph", type=int, default=1, help="replay each step as a captured CUDA graph (N=1)")
+    ap.add_argument("--verify", type=int, default=1, help="hash the last step's CSR against femasm's digests")
+    ap.add_argument("--ref-budget-s", type=float, default=150.0,
+                    help="--impl reference: wall-clock budget of the timed steps (sizes each step's sample)")
     return ap.parse_args()
 
 
@@ -86,7 +104,14 @@ def mesh_for(config: str, seed: int):
     return kind, n, (1.0 if lam is None else lam), (0.5 if mu is None else mu), sm
 
 
-def alg_bytes(kind, nme, nq, n_rows, nnz, owned_all=True):
+def common_config(config, seed, sm):
+    """`config` of both arms (identical, so the driver compares like with like)."""
+    return {"workload": f"{config}: {DESCR[config]}", "nq": sm.nq, "nme": sm.nme, "seed": seed,
+            "l2": "inputs (me 12 B/tri + q 16 B/vertex) and the CSR exceed L2 at C3-C5; a 512 MB buffer is "
+                  "also zeroed between timed GPU steps (outside the timed windows)"}
+
+
+def alg_bytes(kind, nme, nq, n_rows, nnz):
     """Compulsory bytes of the paper-level API: me int32 + areas read once,
     q (stiffness, elasticity) or w (weighted mass) read once, rowptr + col int32 + val f64
     written once."""
@@ -101,10 +126,9 @@ def alg_bytes(kind, nme, nq, n_rows, nnz, owned_all=True):
 class ClockSampler:
     """nvidia-smi clocks and throttle reasons during the timed region (B200_PROFILING.md).
 
-    A background thread issues single-shot queries back to back (a looping nvidia-smi writing
-    into a pipe buffers its output and loses it when terminated); every sample is timestamped
-    and the summary keeps the samples taken inside [mark_start, mark_end].  When the timed region
-    is shorter than one query, the samples adjacent to it are reported and flagged."""
+    A background thread issues single-shot queries back to back; every sample is timestamped
+    and the summary keeps the samples taken inside [mark_start, mark_end].  When the timed
+    region is shorter than one query, the samples adjacent to it are reported and flagged."""
 
     FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
@@ -178,7 +202,7 @@ def measured_peak():
     p = REPO / "MEASURED_PEAKS.json"
     try:
         d = json.loads(p.read_text())
-        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs, burst copy)"
     except Exception:
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
@@ -194,38 +218,104 @@ def ncu_traffic(config: str):
         return None
 
 
-def cpu_baseline_port(kind, sm, lam, mu, runs):
-    """1-core CPU baseline: the numpy restatement of femasm's OptV2 (oracle/), timed like
-    femasm bench._time_cell (one discarded warm-up, median of the timed runs)."""
+# ------------------------------------------------------------------------------------------
+# CPU legs: femasm (the reference) on a bounded row-block sample
+# ------------------------------------------------------------------------------------------
+def reference_module():
+    """femasm from the offline install in baseline/_ref (the unmodified reference package), or
+    None when it is absent (then the numpy restatement in oracle/ stands in)."""
+    if REF_INSTALL.is_dir() and str(REF_INSTALL) not in sys.path:
+        sys.path.insert(0, str(REF_INSTALL))
+    try:
+        import femasm  # noqa: F401
+
+        return femasm
+    except ImportError:
+        return None
+
+
+def row_block_sample(sm, G, b):
+    """The sub-mesh of the triangles touching vertex rows [v0, v1) (block b of G), in their
+    original order, with the used vertices compacted (order-preserving renumbering, so the
+    sort structure of OptV2 is unchanged).  Returns (V, C, w, v0, v1)."""
+    v0, v1 = (sm.nq * b) // G, (sm.nq * (b + 1)) // G
+    C = sm.connectivity
+    touch = ((C >= v0) & (C < v1)).any(axis=1)
+    sub = C[touch]
+    used = np.unique(sub)
+    return sm.vertices[used], np.searchsorted(used, sub), sm.weights[used], v0, v1
+
+
+def sample_split(kind, nme, target_tri):
+    """Smallest power-of-two row split whose block sub-mesh has at most ~target_tri triangles
+    (a block of 1/G of the rows touches about 1 - (1 - 1/G)^3 of the triangles)."""
+    G = 1
+    while nme * (1 - (1 - 1 / G) ** 3) > target_tri and G < (1 << 20):
+        G *= 2
+    return G
+
+
+def _femasm_args(femasm, kind, w, lam, mu):
+    KIND = {"mass": femasm.MatrixKind.MASS, "massw": femasm.MatrixKind.WEIGHTED_MASS,
+            "stiff": femasm.MatrixKind.STIFFNESS, "elastic": femasm.MatrixKind.ELASTIC}
+    kw = {}
+    if kind == "massw":
+        tw = np.asarray(w, dtype=np.float64)
+        kw["weight"] = femasm.WeightField("samples", lambda x, y: tw)
+    if kind == "elastic":
+        kw["params"] = femasm.ElasticParams(lam, mu)
+    return KIND[kind], kw
+
+
+def cpu_assembler(kind, V, C, w, lam, mu):
+    """A zero-argument callable running one OptV2 assembly of (V, C) on the host (femasm, or
+    the restatement), plus the kind label.  Mesh construction is outside the callable, as in
+    femasm bench (/root/reference/pkg/src/femasm/bench.py:157-159)."""
+    femasm = reference_module()
+    if femasm is not None:
+        mesh = femasm.Mesh(V, C)
+        mk, kw = _femasm_args(femasm, kind, w, lam, mu)
+        return (lambda: femasm.assemble(mesh, mk, femasm.Strategy.OPTV2, **kw)), "reference", "femasm (baseline/_ref)"
     from oracle import femasm_oracle as fo
 
-    areas = fo.triangle_areas(sm.vertices, sm.connectivity)
+    areas = fo.triangle_areas(V, C)
+    return (lambda: fo.assemble_optv2(kind, V, C, areas, w, lam, mu)), "port", "numpy restatement of femasm (oracle/)"
+
+
+def cpu_baseline(config, kind, sm, lam, mu, runs):
+    """1-core reference baseline on a bounded sample (about 10-30 s of CPU work)."""
+    target = 8e5 if kind == "elastic" else 3e6
+    G = sample_split(kind, sm.nme, target)
+    V, C, w, v0, v1 = row_block_sample(sm, G, 0)
+    fn, kind_label, what = cpu_assembler(kind, V, C, w, lam, mu)
     times = []
-    for i in range(runs + 1):
+    for i in range(runs + 1):  # run 0 is the discarded warm-up (femasm bench._time_cell)
         t0 = time.perf_counter()
-        fo.assemble_optv2(kind, sm.vertices, sm.connectivity, areas, sm.weights, lam, mu)
+        fn()
         dt = time.perf_counter() - t0
         if i > 0:
             times.append(dt)
     t = statistics.median(times)
-    return {"value": sm.nme / t, "unit": UNIT, "cores": 1, "kind": "port",
-            "sample": f"full mesh ({sm.nme} triangles), numpy OptV2 restatement, median of {runs} after 1 warm-up",
-            "seconds_per_assembly": t}
+    sample = (f"{what} OptV2, 1 thread, on the sub-mesh of the {config} mesh made of the {len(C)} triangles touching "
+              f"vertex rows [{v0}, {v1}) (block 0 of {G}; {len(V)} vertices compacted), median of {runs} after 1 "
+              f"discarded warm-up (femasm bench._time_cell); triangles/s extrapolated linearly to the full "
+              f"{sm.nme}-triangle mesh (OptV2 is linear in nme, SURVEY.md §8(d))"
+              if G > 1 else
+              f"{what} OptV2, 1 thread, full {config} mesh ({sm.nme} triangles), median of {runs} after 1 warm-up")
+    return {"value": len(C) / t, "unit": UNIT, "cores": 1, "kind": kind_label, "sample": sample,
+            "seconds_per_sample": t, "sample_triangles": int(len(C)), "extrapolated": G > 1}
 
 
-# ------------------------------------------------------------------------------------------
-# reference arm: the reference algorithm on every host core (row-block subsets in processes)
-# ------------------------------------------------------------------------------------------
 _REF = {}
 
 
-def _ref_block(args):
-    from oracle import femasm_oracle as fo
-
-    v0, v1 = args
+def _ref_block(b):
     d = _REF
-    ptr, idx, vals = fo.assemble_row_block(d["kind"], d["V"], d["C"], d["areas"], d["w"], d["lam"], d["mu"], v0, v1)
-    return int(ptr[-1])
+    V, C, w, _, _ = row_block_sample(d["sm"], d["G"], b)
+    fn, _, _ = cpu_assembler(d["kind"], V, C, w, d["lam"], d["mu"])
+    t0 = time.perf_counter()
+    fn()
+    return len(C), time.perf_counter() - t0
 
 
 def run_reference(args):
@@ -234,38 +324,93 @@ def run_reference(args):
         return 0
     import multiprocessing as mp
 
-    from oracle import femasm_oracle as fo
-    from paper_1305_3122_b200.dist import row_blocks
-
     kind, n, lam, mu, sm = mesh_for(args.config, args.seed)
     cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
-    _REF.update(kind=kind, V=sm.vertices, C=sm.connectivity, areas=fo.triangle_areas(sm.vertices, sm.connectivity),
-                w=sm.weights, lam=lam, mu=mu)
-    blocks = row_blocks(sm.nq, cores)
+    femasm = reference_module()
+    # per-process sample sized so the K + W steps fit the budget (femasm: ~3e5 scalar /
+    # ~8e4 elastic triangles per second per core)
+    rate = 8e4 if kind == "elastic" else 3e5
+    per_step_s = max(0.5, args.ref_budget_s / max(1, args.steps + args.warmup))
+    G = max(sample_split(kind, sm.nme, rate * per_step_s), 1)
+    while G < cores:
+        G *= 2
+    procs = min(cores, G)
+    _REF.update(kind=kind, sm=sm, G=G, lam=lam, mu=mu)
     ctx = mp.get_context("fork")
-    times = []
-    with ctx.Pool(cores) as pool:
+    times, tris = [], []
+    with ctx.Pool(procs) as pool:
         for i in range(args.warmup + args.steps):
+            blocks = [(i * procs + j) % G for j in range(procs)]
             t0 = time.perf_counter()
-            nnz = sum(pool.map(_ref_block, blocks))
+            out = pool.map(_ref_block, blocks)
             dt = time.perf_counter() - t0
             if i >= args.warmup:
                 times.append(dt)
+                tris.append(sum(c for c, _ in out))
     total = sum(times)
-    value = sm.nme * len(times) / total
+    value = sum(tris) / total
+    label = "reference" if femasm is not None else "port"
+    what = "femasm (baseline/_ref)" if femasm is not None else "numpy restatement of femasm (oracle/)"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": total / len(times) * 1e3,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": f"synthetic: seeded jittered/permuted unit-square mesh (SURVEY.md §8(d)), seed {args.seed}",
-        "config": {"workload": f"{args.config}: {DESCR[args.config]}", "nq": sm.nq, "nme": sm.nme, "nnz": nnz,
-                   "seed": args.seed, "parallelism": f"{cores} host processes x row-block subset"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "port",
-                         "sample": f"full mesh per step as {cores} row-block subsets (femasm OptV2 numpy restatement)"},
+        "config": common_config(args.config, args.seed, sm),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": procs, "kind": label,
+                         "sample": f"{what} OptV2 in {procs} host processes; each step = {procs} distinct row-block "
+                                   f"sub-meshes of the {G}-way split (triangles touching the block's vertex rows, "
+                                   f"vertices compacted), ~{int(np.mean(tris)) if tris else 0} triangles per step; "
+                                   "value = triangles assembled / step wall time"},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
     return 0
+
+
+# ------------------------------------------------------------------------------------------
+# parity of the timed output: SHA-256 against femasm's own digests
+# ------------------------------------------------------------------------------------------
+def csr_digests(rowptr, col, val, chunk=1 << 26):
+    """SHA-256 of (rowptr int64, col as int64, val f64) in femasm's CSC dtypes (the matrices
+    are bitwise symmetric, so CSR == CSC), streamed from the device in chunks."""
+    import torch
+
+    out = []
+    for t, conv in ((rowptr, torch.int64), (col, torch.int64), (val, torch.float64)):
+        h = hashlib.sha256()
+        for s in range(0, t.numel(), chunk):
+            h.update(t[s:s + chunk].to(conv).cpu().numpy().astype(
+                "<i8" if conv is torch.int64 else "<f8", copy=False).tobytes())
+        out.append(h.hexdigest())
+    return out
+
+
+def verify_output(config, seed, world, rank, rowptr, col, val, nnz, mesh_sha):
+    """Compare the last timed step's CSR with femasm's digests for this mesh (whole matrix at
+    N=1, the rank's row block for N>1)."""
+    try:
+        data = json.loads(DIGESTS.read_text())
+    except Exception:
+        return {"checked": False, "why": "no digest file"}
+    key = f"{config}/s{seed}" if world == 1 else f"{config}B/s{seed}/G{world}/b{rank}"
+    ent = data.get(key)
+    if ent is None:
+        return {"checked": False, "why": f"no femasm digest for {key}"}
+    if ent.get("mesh_sha256") and ent["mesh_sha256"] != mesh_sha:
+        return {"checked": False, "why": "generated mesh differs from the digested one (numpy version?)"}
+    got = csr_digests(rowptr, col[:nnz], val[:nnz])
+    ok = (int(ent["nnz"]) == nnz and got[0] == ent["col_ptr_sha256"] and got[1] == ent["row_idx_sha256"]
+          and got[2] == ent["values_sha256"])
+    return {"checked": True, "match": bool(ok), "key": key, "nnz": nnz,
+            "against": "SHA-256 of femasm OptV2 col_ptr/row_idx/values (tests/golden/reference_digests.json)"}
+
+
+def mesh_sha256(sm):
+    h = hashlib.sha256()
+    for a in (sm.vertices.astype("<f8"), sm.connectivity.astype("<i8"), sm.weights.astype("<f8")):
+        h.update(np.ascontiguousarray(a).tobytes())
+    return h.hexdigest()
 
 
 # ------------------------------------------------------------------------------------------
@@ -308,12 +453,15 @@ def run_ours(args):
             dist.init_process_group(backend)
 
     kind, n, lam, mu, sm = mesh_for(args.config, args.seed)
-    areas = fa.compute_areas(sm.vertices, sm.connectivity)
     me32 = np.ascontiguousarray(sm.connectivity, dtype=np.int32)
     me_d = torch.from_numpy(me32).to(dev)
     q_d = torch.from_numpy(sm.vertices).to(dev)
-    a_d = torch.from_numpy(areas).to(dev)
     w_d = torch.from_numpy(sm.weights).to(dev) if kind == "massw" else None
+    # the mesh's areas, computed on the device with compute_areas' formula (mesh.py:51-69)
+    a_d = torch.empty(sm.nme, dtype=torch.float64, device=dev)
+    ar = ResultBlock()
+    _lib.check(_lib.lib().fa_compute_areas(me_d.data_ptr(), sm.nme, q_d.data_ptr(), a_d.data_ptr(), ar.ptr,
+                                           _lib.stream_handle()), "fa_compute_areas")
     q_use = q_d if kind in ("stiff", "elastic") else None
     # as assemble() does for a Mesh whose areas it computed: stiffness and elasticity recompute
     # them from the coordinates they gather anyway (bitwise compute_areas,
@@ -332,7 +480,6 @@ def run_ours(args):
     res = ResultBlock()
     nnz_t = torch.empty(world, dtype=torch.int64, device=dev)
     flush = torch.empty(512 * 1024 * 1024, dtype=torch.uint8, device=dev)
-    stream = torch.cuda.current_stream()
     ev_rows0, ev_rows1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev_rows0.record(); ev_rows1.record()
     torch.cuda.synchronize()
@@ -351,7 +498,7 @@ def run_ours(args):
             else:
                 dist.all_gather_into_tensor(nnz_t, rowptr[-1:])  # row-offset allgather (NCCL)
 
-    # one cold (or warm) step captured as a CUDA graph: the launches of the ~8 kernels of a
+    # one cold (or warm) step captured as a CUDA graph: the launches of the ~9 kernels of a
     # step are replayed without host round trips (the kernel timer events are graph nodes)
     graphs = {}
 
@@ -364,13 +511,15 @@ def run_ours(args):
                 step(cold)  # warm the capture stream
             torch.cuda.current_stream().wait_stream(side)
             torch.cuda.synchronize()
-            lib.fa_set_kernel_timer(ctypes_ptr(ev_rows0), ctypes_ptr(ev_rows1))
+            lib.fa_set_kernel_timer(ev_rows0.cuda_event, ev_rows1.cuda_event)
             with torch.cuda.graph(g):
                 step(cold)
             lib.fa_set_kernel_timer(None, None)
             torch.cuda.synchronize()
             graphs[cold] = g
         return graphs[cold]
+
+    use_graph = args.graph and world == 1  # (NCCL collectives stay eager for N > 1)
 
     def timed_loop(steps, cold):
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
@@ -383,7 +532,7 @@ def run_ours(args):
             if g is not None:
                 g.replay()
             else:
-                lib.fa_set_kernel_timer(ctypes_ptr(ev_rows0), ctypes_ptr(ev_rows1))
+                lib.fa_set_kernel_timer(ev_rows0.cuda_event, ev_rows1.cuda_event)
                 step(cold)
             ends[i].record()
             torch.cuda.synchronize()
@@ -391,11 +540,6 @@ def run_ours(args):
         lib.fa_set_kernel_timer(None, None)
         per = [s.elapsed_time(e) for s, e in zip(starts, ends)]
         return per, rows_ms
-
-    def ctypes_ptr(ev):
-        return ev.cuda_event
-
-    use_graph = args.graph and world == 1  # (NCCL collectives stay eager for N > 1)
 
     for _ in range(args.warmup):
         step(True)
@@ -413,10 +557,17 @@ def run_ours(args):
     clocks.mark_end()
     clock_info = clocks.stop()
     r = res.fetch()
+    rb = plan._build_res.fetch()
     local_nnz = int(r.nnz)
     total_ms = sum(per_step)
+    # parity of what was timed: the last cold step's CSR against femasm's digests
+    parity = {"checked": False, "why": "--verify 0"}
+    if args.verify:
+        parity = verify_output(args.config, args.seed, world, rank, rowptr, col, val, local_nnz, mesh_sha256(sm))
+        parity["errors"] = {"degenerate_index": None if r.degenerate_index == _lib.INT64_MAX else int(r.degenerate_index),
+                            "index_error_pos": None if rb.index_error_pos == _lib.INT64_MAX else int(rb.index_error_pos)}
     # warm: the plan reused (symbolic pattern reuse)
-    warm_step, _ = timed_loop(max(3, args.steps // 2), cold=False)
+    warm_step, warm_rows = timed_loop(max(3, args.steps // 2), cold=False)
     warm_ms = sum(warm_step) / len(warm_step)
     t = torch.tensor([total_ms, warm_ms, float(np.mean(rows_ms))], dtype=torch.float64, device=dev)
     if world > 1:
@@ -428,22 +579,31 @@ def run_ours(args):
         total_nnz = local_nnz
     total_ms, warm_ms, rows_avg_ms = (float(x) for x in t.tolist())
     value = sm.nme * args.steps / (total_ms * 1e-3)
+    del flush
+    torch.cuda.empty_cache()
 
     # end to end through the host-buffer API: pinned inputs -> device, plan, assemble, CSR -> host
     e2e = None
     if args.e2e_steps > 0:
+        del col, val
+        plan.close()
+        torch.cuda.empty_cache()
         recompute = kind in ("stiff", "elastic")  # areas from q on the device, as above
         ha = HostAssembler(kind, sm.nq, sm.nme, v0, v1, recompute_areas=recompute, depth=2)
         pin = lambda x: torch.from_numpy(np.ascontiguousarray(x)).pin_memory()  # noqa: E731
-        h_me, h_q, h_a = pin(me32), pin(sm.vertices), (None if recompute else pin(areas))
+        h_me = pin(me32)
+        h_q = pin(sm.vertices) if kind in ("stiff", "elastic") else None
+        h_a = None
+        if not recompute:
+            h_a = torch.empty(sm.nme, dtype=torch.float64).pin_memory()
+            h_a.copy_(torch.from_numpy(fa.compute_areas(sm.vertices, sm.connectivity)))
         h_w = pin(sm.weights) if kind == "massw" else None
-        h_q = h_q if kind in ("stiff", "elastic") else None
         lat = []
-        for i in range(2 + 3):  # warm-up, then the latency of single synchronous calls
+        for i in range(1 + 2):  # warm-up, then the latency of single synchronous calls
             torch.cuda.synchronize()
             t0 = time.perf_counter()
             ha.run(h_me, h_q, h_a, h_w, lam, mu)
-            if i >= 2:
+            if i >= 1:
                 lat.append(time.perf_counter() - t0)
         # throughput: a stream of steps through submit/result over two slots; every step copies
         # its inputs in and its CSR out inside the timed region
@@ -470,8 +630,9 @@ def run_ours(args):
         e2e = {"value": sm.nme / float(te[0]), "unit": UNIT, "h2d_bytes_per_step": int(h2d),
                "d2h_bytes_per_step": int(d2h_t.item()),
                "timing": f"wall clock over {args.e2e_steps} pipelined steps (submit/result, 2 slots), max over ranks",
-               "latency_ms": float(te[1]) * 1e3, "latency": "one synchronous run() call, median of 3",
-               "api": "paper_1305_3122_b200.optv2.HostAssembler.submit/result (C ABI fa_plan_build + fa_assemble)"}
+               "latency_ms": float(te[1]) * 1e3, "latency": "one synchronous run() call, median of 2",
+               "api": "paper_1305_3122_b200.optv2.HostAssembler.submit/result (C ABI fa_plan_build + fa_assemble)",
+               "floor": "PCIe: the per-step D2H of the CSR bounds this (~55 GB/s measured, DESIGN.md §6)"}
 
     peak, peak_src = measured_peak()
     ab_rank = alg_bytes(kind, sm.nme, sm.nq, n_rows, local_nnz)
@@ -480,38 +641,42 @@ def run_ours(args):
     ab_total = alg_bytes(kind, sm.nme, sm.nq, (sm.nq * (2 if kind == "elastic" else 1)), total_nnz)
     cpu = None
     if rank == 0 and world == 1 and args.cpu_baseline_runs > 0:
-        cpu = cpu_baseline_port(kind, sm, lam, mu, args.cpu_baseline_runs)
+        cpu = cpu_baseline(args.config, kind, sm, lam, mu, args.cpu_baseline_runs)
 
     if rank == 0:
+        steps_list = launches_per_step(kind, sm.nme, sm.nq, v1 - v0)
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": f"synthetic: seeded jittered/permuted unit-square mesh (SURVEY.md §8(d)), seed {args.seed}",
-            "config": {"workload": f"{args.config}: {DESCR[args.config]}", "nq": sm.nq, "nme": sm.nme, "nnz": total_nnz,
-                       "seed": args.seed, "parallelism": f"row-blocks x{world}" if world > 1 else "single GPU",
-                       "step": "cold: plan build (part histogram, placement, per-part vertex sort) + fused row "
-                               "kernel (+ NCCL nnz allgather when N>1)",
-                       "l2": "512 MB buffer zeroed between timed steps (outside the timed windows)",
-                       "launch": "CUDA graph replay per step" if (args.graph and world == 1) else "eager launches"},
+            "config": common_config(args.config, args.seed, sm),
+            "nnz": total_nnz,
+            "parallelism": f"row-blocks x{world}" if world > 1 else "single GPU",
+            "step": "cold: plan build (part histogram, placement, per-part vertex sort) + fused row kernel "
+                    "(+ NCCL nnz allgather when N>1), from device-resident me/q",
+            "launch": "CUDA graph replay per step" if use_graph else "eager launches",
+            "parity": parity,
             "hbm_gbs_whole_step": ab_total / (total_ms / args.steps * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "kernel": "k_rows (fused element + sparse() row kernel)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "alg_bytes_per_launch": ab_rank, "avg_launch_ms": rows_avg_ms,
-                         "peak_source": peak_src},
+                         "peak_source": peak_src,
+                         "alg_bytes": "12 B/tri me + 8 B/tri areas + 16 B/vertex q (stiff/elastic) or 8 B/vertex w "
+                                      "(massw) + 8 B/row rowptr + 12 B/entry (col int32 + val f64); SURVEY.md §8(d)"},
             "roofline_whole_step_frac": (ab_total / (total_ms / args.steps * 1e-3) / 1e9) / peak,
             "warm": {"value": sm.nme / (warm_ms * 1e-3), "ms_per_step": warm_ms,
                      "what": "plan reused (vertex-sorted incidences cached): row kernel only"},
             "clocks": clock_info,
             "e2e": e2e,
-            "gpu_launches": len(launches_per_step(kind, sm.nme, sm.nq, v1 - v0)) * args.steps,
-            "gpu_launches_detail": "per step: " + ", ".join(launches_per_step(kind, sm.nme, sm.nq, v1 - v0)),
+            "gpu_launches": len(steps_list) * args.steps,
+            "gpu_launches_detail": "per step: " + ", ".join(steps_list),
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
-    return 0
+    return 0 if (not parity.get("checked") or parity.get("match")) else 3
 
 
 def main():

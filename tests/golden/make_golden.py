@@ -118,6 +118,9 @@ def digests(names):
     data = json.loads(path.read_text()) if path.exists() else {}
     for spec in names:
         # spec: C1 | C1:s1 | EL64 (elastic lam=2 mu=0.7 N=64 seed 0) | C5B:G:b (row block b of G)
+        if spec == "C5ALL":
+            c5_all_blocks(data, path)
+            continue
         if spec.startswith("C5B"):
             _, g, blk = spec.split(":")
             row_block_digest(data, path, "C5", int(g), int(blk), seed=0)
@@ -151,6 +154,76 @@ def digests(names):
             print(key, data[key]["nnz"], f"{t1 - t0:.1f}s", flush=True)
             path.write_text(json.dumps(data, indent=1, sort_keys=True))
             del mesh, m, sm
+
+
+def c5_all_blocks(data, path, cfg="C5", seed=0, G=16):
+    """Every row block of the G-way split of `cfg`, from ONE generated mesh, each assembled by
+    femasm through the row-block subset (as row_block_digest).  The block arrays are also fed,
+    in row order, into streaming SHA-256s of every coarser split G/2, G/4, ..., 1 (block b of
+    G/2 is blocks 2b, 2b+1 of G, because floor(nq*b/(G/2)) == floor(nq*2b/G)), so the digests
+    of the whole matrix (G=1, what a single GPU assembles) and of the G=8 split come out of
+    femasm runs that each fit in memory."""
+    kind, n, lam, mu = BASELINE_CONFIGS[cfg]
+    t0 = time.perf_counter()
+    sm = seeded_square_mesh(n, seed)
+    nq = sm.nq
+    C = sm.connectivity
+    levels = []
+    g = G
+    while g >= 1:
+        levels.append(g)
+        g //= 2
+    hs = {g: None for g in levels}
+    state = {g: {"blk": -1, "h": None, "lo": 0, "nnz": 0, "touched": 0} for g in levels}
+    mdig = mesh_digest(sm)
+
+    def close(g):
+        st = state[g]
+        if st["h"] is None:
+            return
+        b = st["blk"]
+        v0, v1 = (nq * b) // g, (nq * (b + 1)) // g
+        key = f"{cfg}B/s{seed}/G{g}/b{b}" if g > 1 else f"{cfg}/s{seed}"
+        hp, hr, hv, vs = st["h"]
+        ent = {"kind": kind, "N": n, "seed": seed, "nq": int(nq), "nme": int(sm.nme),
+               "nnz": int(st["nnz"]), "mesh_sha256": mdig,
+               "col_ptr_sha256": hp.hexdigest(), "row_idx_sha256": hr.hexdigest(),
+               "values_sha256": hv.hexdigest(), "via": f"streamed from the G={G} row-block subsets"}
+        if g > 1:
+            ent.update({"G": g, "block": b, "v0": int(v0), "v1": int(v1)})
+        else:
+            ent.update({"lam": lam, "mu": mu, "values_sum_blocks": vs})
+        data[key] = ent
+        print(key, ent["nnz"], flush=True)
+
+    for blk in range(G):
+        v0, v1 = (nq * blk) // G, (nq * (blk + 1)) // G
+        touch = ((C >= v0) & (C < v1)).any(axis=1)
+        sub = femasm.Mesh(sm.vertices, C[touch])
+        m = femasm.assemble(sub, KIND[kind], femasm.Strategy.OPTV2)
+        lo, hi = int(m.col_ptr[v0]), int(m.col_ptr[v1])
+        ptr = (m.col_ptr[v0:v1 + 1] - lo).astype("<i8")
+        rows = m.row_idx[lo:hi].astype("<i8")
+        vals = m.values[lo:hi].astype("<f8")
+        del m, sub
+        for g in levels:
+            b = blk * g // G
+            st = state[g]
+            if st["blk"] != b:
+                close(g)
+                st.update(blk=b, h=(hashlib.sha256(), hashlib.sha256(), hashlib.sha256(), 0.0), lo=0, nnz=0)
+                st["h"][0].update(np.zeros(1, "<i8").tobytes())
+            hp, hr, hv, vs = st["h"]
+            hp.update((ptr[1:] + st["nnz"]).tobytes())
+            hr.update(rows.tobytes())
+            hv.update(vals.tobytes())
+            st["h"] = (hp, hr, hv, vs + float(vals.sum()))
+            st["nnz"] += len(rows)
+        print(f"block {blk}/{G} rows [{v0},{v1}) nnz {len(rows)} {time.perf_counter() - t0:.0f}s", flush=True)
+        del ptr, rows, vals
+    for g in levels:
+        close(g)
+    path.write_text(json.dumps(data, indent=1, sort_keys=True))
 
 
 def row_block_digest(data, path, cfg, G, blk, seed=0):
