@@ -169,6 +169,27 @@ int fa_triplets_to_csc(const int64_t* d_rows, const int64_t* d_cols, const doubl
                        int64_t* d_rowidx, double* d_vals_out, void* d_workspace,
                        size_t workspace_bytes, fa_result* d_result, void* stream);
 
+/* fa_triplets_to_csc with flags.  FA_TRIPLETS_KEEP_ZEROS gives the reference CscBuilder's
+ * semantics (sparse.py:208-290, used by the CLASSICAL / OPTV0 element loops,
+ * assembly.py:359-375): every position a triplet names is stored - input zeros and zero sums
+ * included - and each position's sum starts from its first value (`aa[pos] += v`). */
+#define FA_TRIPLETS_KEEP_ZEROS 1
+int fa_triplets_to_csc_ex(const int64_t* d_rows, const int64_t* d_cols, const double* d_vals,
+                          int64_t len, int64_t n_rows, int64_t n_cols, int flags, int64_t* d_colptr,
+                          int64_t* d_rowidx, double* d_vals_out, void* d_workspace,
+                          size_t workspace_bytes, fa_result* d_result, void* stream);
+
+/* Element-loop strategies CLASSICAL / OPTV0 / OPTV1 (assembly.py:359-397): the triplets of
+ * every triangle's element matrix computed with the per-element formulas of elements.py:34-154
+ * (elem_mass, elem_mass_weighted, elem_stiff, elem_stiff_elastic - rounded differently from the
+ * batch kernels), in triangle-major order: position k*r + a + order*b holds entry (a, b) of
+ * triangle k, order 3 (r = 9) or 6 (ELASTIC, r = 36, interleaved dofs).  d_rows/d_cols int64,
+ * d_vals f64, r*nme each.  A triangle with area <= 1e-300 is reported in d_result. */
+int fa_element_triplets(int kind, const int32_t* d_me, int64_t nme, const double* d_q,
+                        const double* d_areas, const double* d_w, double lam, double mu,
+                        int64_t* d_rows, int64_t* d_cols, double* d_vals, fa_result* d_result,
+                        void* stream);
+
 /* CSC (col_ptr, row_idx int64; values f64; host arrays) -> coordinate MatrixMarket file, byte
  * identical to femasm's write_matrix_market (pkg/src/femasm/sparse.py:332-339): 1-based "i j v"
  * lines in CSC order, values "%.17g".  threads <= 0: all hardware threads.  Host only. */

@@ -26,6 +26,8 @@ FA_ERR_LENGTH = 6
 
 KIND_CODES = {"mass": 0, "massw": 1, "stiff": 2, "elastic": 3}
 
+FA_TRIPLETS_KEEP_ZEROS = 1  # CscBuilder semantics (include/femasm_b200.h)
+
 INT64_MAX = np.iinfo(np.int64).max
 
 # Every symbol include/femasm_b200.h declares (checked by tests/test_boundary.py).
@@ -46,6 +48,8 @@ EXPORTED_SYMBOLS = (
     "fa_compute_areas",
     "fa_triplets_workspace",
     "fa_triplets_to_csc",
+    "fa_triplets_to_csc_ex",
+    "fa_element_triplets",
     "fa_selftest_division",
     "fa_set_kernel_timer",
     "fa_write_matrix_market",
@@ -102,6 +106,8 @@ _SIGNATURES = {
     "fa_compute_areas": (_I, [_P, _I64, _P, _P, _P, _P]),
     "fa_triplets_workspace": (ctypes.c_size_t, [_I64, _I64, _I64]),
     "fa_triplets_to_csc": (_I, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, ctypes.c_size_t, _P, _P]),
+    "fa_triplets_to_csc_ex": (_I, [_P, _P, _P, _I64, _I64, _I64, _I, _P, _P, _P, _P, ctypes.c_size_t, _P, _P]),
+    "fa_element_triplets": (_I, [_I, _P, _I64, _P, _P, _P, _D, _D, _P, _P, _P, _P, _P]),
     "fa_selftest_division": (_I, [_I64, ctypes.c_uint64, _P, _P, _P]),
     "fa_set_kernel_timer": (_I, [_P, _P]),
     "fa_write_matrix_market": (_I, [ctypes.c_char_p, _I64, _I64, _P, _P, _P, _I]),

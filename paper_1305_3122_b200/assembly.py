@@ -269,6 +269,37 @@ def assemble_device(mesh: Mesh, kind: MatrixKind, *, weight=None, params=None, p
     return rowptr, col, val, r
 
 
+def _assemble_element_loop(mesh: Mesh, kind: MatrixKind, weight, params, keep_zeros: bool) -> CscMatrix:
+    """The element-loop strategies on the GPU (assembly.py:359-397): every triangle's element
+    matrix from the per-element formulas of elements.py (fa_element_triplets), then either
+    CscBuilder semantics (CLASSICAL / OPTV0: every touched position stored, explicit zeros
+    kept, sums starting from their first value, sparse.py:208-290) or Matlab sparse() (OPTV1:
+    _assemble_triplet_loop -> csc_from_triplets, sparse.py:140-189)."""
+    from .sparse import _triplets_device
+
+    torch = require_cuda()
+    dev = device()
+    me, q, areas = mesh.device_arrays()
+    order = 6 if kind is MatrixKind.ELASTIC else 3
+    n_trip = order * order * mesh.nme
+    rows = torch.empty(n_trip, dtype=torch.int64, device=dev)
+    cols = torch.empty(n_trip, dtype=torch.int64, device=dev)
+    vals = torch.empty(n_trip, dtype=torch.float64, device=dev)
+    w_dev = to_device(weight.sample(mesh)) if kind is MatrixKind.WEIGHTED_MASS else None
+    lam = params.lam if kind is MatrixKind.ELASTIC else 0.0
+    mu = params.mu if kind is MatrixKind.ELASTIC else 0.0
+    res = ResultBlock()
+    rc = _lib.lib().fa_element_triplets(_kind_code(kind), me.data_ptr(), mesh.nme, q.data_ptr(), areas.data_ptr(),
+                                        _lib.ptr(w_dev), lam, mu, rows.data_ptr(), cols.data_ptr(), vals.data_ptr(),
+                                        res.ptr, _lib.stream_handle())
+    _lib.check(rc, "fa_element_triplets")
+    r = res.fetch()
+    if r.degenerate_index != _lib.INT64_MAX:  # elements.py:27-31 (_check_area)
+        raise ValueError(f"triangle area must be positive, got {float(mesh.areas[r.degenerate_index]):g}")
+    n = kind.n_dof(mesh.nq)
+    return _triplets_device(rows, cols, vals, n, n, keep_zeros=keep_zeros)
+
+
 def assemble(
     mesh: Mesh,
     kind: MatrixKind,
@@ -280,10 +311,12 @@ def assemble(
 ) -> CscMatrix:
     """Assemble the global matrix of ``kind`` over ``mesh`` (assembly.py:419-452).
 
-    ``weight`` is required for WEIGHTED_MASS, ``params`` for ELASTIC.  All strategies run
-    the fused GPU OptV2 path; the element-loop strategies (CLASSICAL, OPTV0, OPTV1) honour
-    ``budget_s`` as a cooperative limit checked before launching (AssemblyBudgetExceeded),
-    OPTV2 ignores it, as in the reference.
+    ``weight`` is required for WEIGHTED_MASS, ``params`` for ELASTIC.  OPTV2 runs the fused
+    GPU path (plan + row kernel).  The element-loop strategies keep the reference's
+    semantics on the GPU: per-element formulas (elements.py), CLASSICAL / OPTV0 with the
+    CscBuilder's explicit zeros, OPTV1 through Matlab sparse(); they honour ``budget_s`` as
+    a cooperative limit checked before launching (AssemblyBudgetExceeded); OPTV2 ignores
+    it, as in the reference.
     """
     _check_kind_args(kind, weight, params)
     t0 = time.perf_counter()
@@ -291,6 +324,9 @@ def assemble(
         elapsed = time.perf_counter() - t0
         if elapsed > budget_s or budget_s <= 0.0:
             raise AssemblyBudgetExceeded(max(elapsed, 0.0), 0, mesh.nme)
-    rowptr, col, val, _ = assemble_device(mesh, kind, weight=weight, params=params)
-    n = kind.n_dof(mesh.nq)
-    return CscMatrix.from_device(n, n, rowptr, col, val)
+    if strategy is Strategy.OPTV2:
+        rowptr, col, val, _ = assemble_device(mesh, kind, weight=weight, params=params)
+        n = kind.n_dof(mesh.nq)
+        return CscMatrix.from_device(n, n, rowptr, col, val)
+    return _assemble_element_loop(mesh, kind, weight, params,
+                                  keep_zeros=strategy in (Strategy.CLASSICAL, Strategy.OPTV0))

@@ -42,8 +42,7 @@
 //     K6 compact     only when a scalar-kind sum was exactly zero (Matlab drops it,
 //                    sparse.py:177-179): removes those entries in place, bucket by bucket.
 // Rows of degree > MAXD (and every row of a bucket whose incidences exceed CAPB) use an
-// O(d^2) general path with the same summation order.  Build-time knobs (experiments):
-// FA_ROWS_AU, FA_ROWS_MINB, FA_CAPB, FA_BV; FA_EXP_TIMELINE records per-block phase times.
+// O(d^2) general path with the same summation order.
 #include <climits>
 #include <cstdlib>
 #include <new>
@@ -51,43 +50,18 @@
 #include "fa_common.cuh"
 #include "fa_element.cuh"
 
-#ifndef FA_ROWS_MINB_E
-#define FA_ROWS_MINB_E 2
-#endif
-#ifndef FA_ROWS_AU_E
-#define FA_ROWS_AU_E 1  // elasticity (12 values per incidence)
-#endif
-#ifndef FA_ROWS_AU
-#define FA_ROWS_AU 3  // mass, stiffness: incidences in flight per thread in the row kernel phase a
-#endif
-#ifndef FA_ROWS_AU_W
-#define FA_ROWS_AU_W 3  // weighted mass: W records in flight per thread (no spills at 96 registers)
-#endif
-#ifndef FA_ROWS_MINB_W
-#define FA_ROWS_MINB_W 5  // weighted mass: <= 102 registers (no gather reuse, L1 matters less)
-#endif
-#ifndef FA_ROWS_MINB
-#define FA_ROWS_MINB 4  // mass, stiffness: <= 128 registers, no local memory
-#endif
-
 namespace fa {
 
-#ifndef FA_BV
-#define FA_BV 128
-#endif
-constexpr int BV = FA_BV;          // vertices per row bucket
-#ifndef FA_CAPB_E
-#define FA_CAPB_E (7 * BV)  // elasticity: 12 values per incidence, two blocks per SM
-#endif
-#ifndef FA_CAPB
-#define FA_CAPB (8 * BV)
-#endif
-#ifndef FA_CAPB_W
-// weighted mass (five blocks per SM): a smaller bucket leaves L1 more room; the mean degree of
-// a planar triangulation is below 6, so overflowing buckets (general path) stay rare
-#define FA_CAPB_W (7 * BV)
-#endif
-constexpr int CAPB = FA_CAPB;      // incidences per bucket held in shared memory
+constexpr int BV = 128;            // vertices per row bucket
+// row kernel shape per kind: incidences held in shared memory per bucket (CAP), blocks per SM
+// (register budget), incidences / W records in flight per thread in phase a (AU)
+constexpr int CAPB = 8 * BV;       // mass, stiffness: <= 128 registers, four blocks per SM
+constexpr int CAPB_E = 7 * BV;     // elasticity: 12 values per incidence, two blocks per SM
+// weighted mass (five blocks per SM, <= 102 registers): a smaller bucket leaves L1 more room; the
+// mean degree of a planar triangulation is below 6, so overflowing buckets (general path) stay rare
+constexpr int CAPB_W = 7 * BV;
+constexpr int ROWS_MINB = 4, ROWS_MINB_W = 5, ROWS_MINB_E = 2;
+constexpr int ROWS_AU = 3, ROWS_AU_W = 3, ROWS_AU_E = 1;
 constexpr int MAXD = 8;            // incidences per row on the register fast path
 constexpr int PLOG0 = 10;          // log2 of the minimum part size (vertices)
 constexpr int MAX_PARTS = 8192;
@@ -95,16 +69,13 @@ constexpr int PLAN_THREADS = 1024;
 constexpr int SORT_THREADS = 512;   // k_part_sort (2 blocks / SM, 64 registers)
 constexpr int PLACE_THREADS = 1024;  // k_part_hist / k_part_place block size
 constexpr int PLACE_BLOCKS_PER_SM = 1;
-#ifndef FA_PLACE_TRI
-#define FA_PLACE_TRI 2048
-#endif
-constexpr int PLACE_TRI = FA_PLACE_TRI;  // triangles per placement round
+constexpr int PLACE_TRI = 2048;    // triangles per placement round
 constexpr int SPLIT_MIN = 8192;    // fine parts above which placement goes through coarse parts
 // records above this size do not stay in L2 between placement and sort, so the placement's
 // runs must be long (coarse parts) and a parallel split regroups them by fine part
 constexpr int64_t SPLIT_BYTES = int64_t(160) << 20;
 constexpr int SPLIT_COARSE = 256;  // coarse parts of a two-level plan (at most)
-constexpr int FINE_HIST_MAX = 49152;  // fine parts counted in k_part_hist's shared memory
+constexpr int FINE_HIST_MAX = 98304;  // fine parts counted in k_part_hist's shared memory (16 bit)
 constexpr int SPLIT2_LOCAL = 1024;    // fine parts a k_part_split round ranks in shared memory
 constexpr int SORT_CAP = 7680;     // part incidences sorted in shared memory (2 blocks / SM)
 
@@ -115,29 +86,7 @@ __global__ void k_reset(fa_result* r, unsigned* z32, int64_t n32, uint64_t* z64,
     const int64_t stride = int64_t(gridDim.x) * blockDim.x;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n32; i += stride) z32[i] = 0;
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < n64; i += stride) z64[i] = 0;
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        r->nnz = 0;
-        r->degenerate_index = INT64_MAX;
-        r->index_error_pos = INT64_MAX;
-        r->col_error_pos = INT64_MAX;
-        r->dropped = 0;
-        r->heavy_rows = 0;
-        r->reserved[0] = 0;
-        r->repeat_error_pos = INT64_MAX;
-    }
-}
-
-__global__ void k_reset_result(fa_result* r) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        r->nnz = 0;
-        r->degenerate_index = INT64_MAX;
-        r->index_error_pos = INT64_MAX;
-        r->col_error_pos = INT64_MAX;
-        r->dropped = 0;
-        r->heavy_rows = 0;
-        r->reserved[0] = 0;
-        r->repeat_error_pos = INT64_MAX;
-    }
+    if (threadIdx.x == 0 && blockIdx.x == 0) reset_result_fields(r);
 }
 
 __device__ __forceinline__ void load_tri_ids(const int32_t* me, int64_t k, int& c0, int& c1, int& c2) {
@@ -192,10 +141,7 @@ __device__ __forceinline__ void tri_wt_store(double4* Wt, int64_t k, double ar, 
 __device__ __noinline__ void hist_tri_wt(const PlanArgs& P, int64_t k0, int64_t k1) {
     const uint64_t pol = l2_evict_first_policy();
     const uint64_t keep = l2_evict_last_policy();
-#ifndef FA_HIST_WT_U
-#define FA_HIST_WT_U 2
-#endif
-    constexpr int U = FA_HIST_WT_U;  // triangles in flight per thread
+    constexpr int U = 2;  // triangles in flight per thread
     for (int64_t k0u = k0 + threadIdx.x; k0u < k1; k0u += U * PLACE_THREADS) {
         int c[U][3];
         double ar[U], wc[U][3];
@@ -227,17 +173,31 @@ __device__ __noinline__ void hist_tri_wt(const PlanArgs& P, int64_t k0, int64_t 
 }
 
 // K1: owned incidences per (block, part) and per part; index validation (sparse.py:131-137 semantics: first bad
-// position in the flattened connectivity).
+// position in the flattened connectivity).  Two-level plans count the fine parts (the coarse counts are their
+// sums) in 16-bit counters packed two per shared word, so up to FINE_HIST_MAX fine parts fit (C5: 65,553); a
+// counter that wraps hands 65536 to the global fine count and to the block's coarse count and takes its carry
+// back out of its neighbour.  Beyond FINE_HIST_MAX fine parts the fine counts go to global atomics and shared
+// memory keeps the coarse ones.
+__device__ __forceinline__ void hist_fine16(unsigned* s_cnt, unsigned* g_fine, unsigned* s_cwrap, unsigned f,
+                                            int fine_per_coarse_log2) {
+    const unsigned sh = (f & 1u) * 16u;
+    const unsigned old = atomicAdd(&s_cnt[f >> 1], 1u << sh);
+    if (((old >> sh) & 0xffffu) == 0xffffu) {  // wrapped
+        if (sh == 0) atomicSub(&s_cnt[f >> 1], 1u << 16);
+        atomicAdd(&g_fine[f], 65536u);
+        atomicAdd(&s_cwrap[f >> fine_per_coarse_log2], 1u);
+    }
+}
+
 __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_constant__ PlanArgs P) {
     pdl_enter();
     extern __shared__ unsigned s_cnt[];
-    // counted per fine part in a two-level plan (the coarse counts are their sums); beyond
-    // FINE_HIST_MAX fine parts the fine counts go to global memory and shared memory keeps
-    // the coarse ones
-    const bool fs = P.fine_hist && !P.fine_global;
-    const int hlog = fs ? P.plog_f : P.plog, hn = fs ? P.nparts_f : P.nparts;
+    const bool fs = P.fine_hist && !P.fine_global;  // fine counts in shared memory (16 bit)
+    const int hn = fs ? (P.nparts_f + 1) / 2 : P.nparts;
     __shared__ unsigned s_tn;
+    __shared__ unsigned s_cwrap[SPLIT_COARSE];  // wrapped fine counters per coarse part
     for (int i = threadIdx.x; i < hn; i += PLACE_THREADS) s_cnt[i] = 0;
+    for (int i = threadIdx.x; i < SPLIT_COARSE; i += PLACE_THREADS) s_cwrap[i] = 0;
     if (threadIdx.x == 0) s_tn = 0;
     __syncthreads();
     const int64_t k0 = int64_t(blockIdx.x) * P.chunk, k1 = min(P.nme, k0 + P.chunk);
@@ -264,7 +224,6 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
                     P.tri[k0 + atomicAdd(&s_tn, 1u)] =
                         make_uint4(unsigned(k), unsigned(c[u][0]), unsigned(c[u][1]), unsigned(c[u][2]));
             }
-#pragma unroll
             if (c[u][0] == c[u][1] || c[u][1] == c[u][2] || c[u][0] == c[u][2])  // first repeating corner
                 atomic_min_i64(&P.res->repeat_error_pos, 3 * k + (c[u][0] == c[u][1] ? 1 : 2));
 #pragma unroll
@@ -272,8 +231,13 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
                 const int64_t v = c[u][a];
                 if (v < 0 || v >= P.nq) atomic_min_i64(&P.res->index_error_pos, 3 * k + a);
                 if (ok && v >= P.v0 && v < P.v1) {
-                    atomicAdd(&s_cnt[(v - P.v0) >> hlog], 1u);
-                    if (P.fine_global) atomicAdd(&P.part_off_f[(v - P.v0) >> P.plog_f], 1u);
+                    const unsigned vl = unsigned(v - P.v0);
+                    if (fs) {
+                        hist_fine16(s_cnt, P.part_off_f, s_cwrap, vl >> P.plog_f, P.plog - P.plog_f);
+                    } else {
+                        atomicAdd(&s_cnt[vl >> P.plog], 1u);
+                        if (P.fine_global) atomicAdd(&P.part_off_f[vl >> P.plog_f], 1u);
+                    }
                 }
             }
         }
@@ -282,6 +246,7 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
     if (P.Wt) hist_tri_wt(P, k0, k1);
     if (P.tri && threadIdx.x == 0) P.tri_cnt[blockIdx.x] = s_tn;
     unsigned* row = P.M + int64_t(blockIdx.x) * P.nparts;
+    auto fine = [&](int f) { return (s_cnt[f >> 1] >> ((f & 1) * 16)) & 0xffffu; };
     if (!P.fine_hist) {
         for (int i = threadIdx.x; i < P.nparts; i += PLACE_THREADS) {
             row[i] = s_cnt[i];
@@ -290,12 +255,16 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
     } else if (P.fine_global) {
         for (int i = threadIdx.x; i < P.nparts; i += PLACE_THREADS) row[i] = s_cnt[i];
     } else {
-        for (int i = threadIdx.x; i < P.nparts_f; i += PLACE_THREADS)
-            if (s_cnt[i]) atomicAdd(&P.part_off_f[i], s_cnt[i]);
+        for (int i = threadIdx.x; i < P.nparts_f; i += PLACE_THREADS) {
+            const unsigned c = fine(i);
+            if (c) atomicAdd(&P.part_off_f[i], c);
+        }
+        // coarse counts of this block (the placement's count-matrix row): sums of its fine
+        // counts plus 65536 per wrapped fine counter
         const int F = 1 << (P.plog - P.plog_f);
         for (int pc = threadIdx.x; pc < P.nparts; pc += PLACE_THREADS) {
-            unsigned c = 0;
-            for (int f = pc * F; f < min((pc + 1) * F, P.nparts_f); ++f) c += s_cnt[f];
+            unsigned c = 65536u * s_cwrap[pc];
+            for (int f = pc * F; f < min((pc + 1) * F, P.nparts_f); ++f) c += fine(f);
             row[pc] = c;
         }
     }
@@ -783,9 +752,9 @@ struct KindTraits {
     // entries of its two dof rows (own, n1, n2 vertex columns, x and y)
     static constexpr int RVALS = KIND == FA_KIND_ELASTIC ? 12 : 3;
     static constexpr int MIN_BLOCKS =
-        KIND == FA_KIND_ELASTIC ? FA_ROWS_MINB_E : (KIND == FA_KIND_MASSW ? FA_ROWS_MINB_W : FA_ROWS_MINB);
+        KIND == FA_KIND_ELASTIC ? ROWS_MINB_E : (KIND == FA_KIND_MASSW ? ROWS_MINB_W : ROWS_MINB);
     static constexpr int CAP =  // incidences in shared memory
-        KIND == FA_KIND_ELASTIC ? FA_CAPB_E : (KIND == FA_KIND_MASSW ? FA_CAPB_W : CAPB);
+        KIND == FA_KIND_ELASTIC ? CAPB_E : (KIND == FA_KIND_MASSW ? CAPB_W : CAPB);
     static constexpr size_t REC_BYTES = size_t(CAP) * (RVALS * 8 + 12);
     static constexpr int STAGE = int(REC_BYTES / 12);  // staged entries fitting the records area
 };
@@ -806,12 +775,6 @@ template <int KIND>
 __device__ __forceinline__ Gathered gather_incidence(const RowsArgs& A, unsigned k, unsigned n1, unsigned n2,
                                                      uint64_t pol) {
     Gathered g;
-#ifdef FA_EXP_NOGATHER
-    g.p1 = make_double2(double(n1), 1.0); g.p2 = make_double2(double(n2), 2.0);
-    g.w1 = double(n1 + 1); g.w2 = double(n2 + 1); g.ar = double(k + 1) * 1e-6;
-    g.wt = make_double4(double(k + 1), double(k + 2), double(k + 3), 0.0);
-    return g;
-#endif
     g.p1 = g.p2 = make_double2(0.0, 0.0);
     g.w1 = g.w2 = 0.0;
     g.ar = (KIND != FA_KIND_MASSW && A.areas) ? ld_keep_f64(A.areas + k, pol) : 0.0;
@@ -868,10 +831,11 @@ __device__ __forceinline__ void incidence_values(const RowsArgs& A, unsigned k, 
         // (assembly.py:251-254) taken in local order - the same operand pairs, so the same bits
         // - and row a is their dot products over 4*area (stiff_entry without the selects)
         const double2 eo = dsub2(g.p1, g.p2), e1 = dsub2(g.p2, own_p), e2 = dsub2(own_p, g.p1);
-        const double a4 = FMUL(4.0, ar);
-        out[0] = FDIV(FADD(FADD(0.0, FMUL(eo.x, eo.x)), FMUL(eo.y, eo.y)), a4);
-        out[1] = FDIV(FADD(FADD(0.0, FMUL(eo.x, e1.x)), FMUL(eo.y, e1.y)), a4);
-        out[2] = FDIV(FADD(FADD(0.0, FMUL(eo.x, e2.x)), FMUL(eo.y, e2.y)), a4);
+        // three true divisions by a4 = 4*area sharing one correctly rounded reciprocal (div_by)
+        const DivBy d4 = div_prepare(FMUL(4.0, ar));
+        out[0] = div_by(d4, FADD(FADD(0.0, FMUL(eo.x, eo.x)), FMUL(eo.y, eo.y)));
+        out[1] = div_by(d4, FADD(FADD(0.0, FMUL(eo.x, e1.x)), FMUL(eo.y, e1.y)));
+        out[2] = div_by(d4, FADD(FADD(0.0, FMUL(eo.x, e2.x)), FMUL(eo.y, e2.y)));
     } else {
         // gradients of the own corner and the two neighbours from the edges opposite them (the
         // reference's u, v, w in local order: same operands, same bits, assembly.py:195-211)
@@ -1031,17 +995,6 @@ __device__ __noinline__ RowCount general_row(const RowsArgs& A, BucketRecs R, bo
     return RowCount{count, zeros};
 }
 
-#ifdef FA_EXP_TIMELINE
-__device__ unsigned long long g_tl[16384 * 6];
-__device__ __forceinline__ unsigned long long gtimer() {
-    unsigned long long t;
-    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-    return t;
-}
-#define TL(b, i) do { if (threadIdx.x == 0 && (b) < 16384) g_tl[(b) * 6 + (i)] = gtimer(); } while (0)
-#else
-#define TL(b, i) do { } while (0)
-#endif
 
 // Sorted candidate columns of a fast row: (neighbour << 4 | slot), slot = 2 * incidence +
 // (0: n1, 1: n2), unused keys 0xffffffff.
@@ -1159,7 +1112,6 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     const uint64_t pol_first = l2_evict_first_policy();
     const uint64_t pol_last = l2_evict_last_policy();
     const int64_t b = next_tile(A.ticket, &s_tile);  // bucket, in launch order
-    TL(b, 0);
     const int64_t nvl = A.v1 - A.v0;
     const int64_t vb0 = b * BV;  // first vertex of the bucket (row-block local)
     const int nvb = int(min(int64_t(BV), nvl - vb0));
@@ -1250,12 +1202,11 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         excl = block_exclusive_scan_1b<NT>(count, s_warp, total);
         lookback_publish(A.status, b, uint64_t(total));
     }
-    TL(b, 1);
 
     // ---- a) per incidence (balanced over threads): gathers from the L2-resident arrays, the
     //         row of the element matrix -> shared memory
     {
-        constexpr int AU = KIND == FA_KIND_ELASTIC ? FA_ROWS_AU_E : (KIND == FA_KIND_MASSW ? FA_ROWS_AU_W : FA_ROWS_AU);
+        constexpr int AU = KIND == FA_KIND_ELASTIC ? ROWS_AU_E : (KIND == FA_KIND_MASSW ? ROWS_AU_W : ROWS_AU);
         for (int i0 = tid; i0 < n; i0 += NT * AU) {
             unsigned ka[AU];
             Gathered g[AU];
@@ -1283,7 +1234,6 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         }
     }
     const bool any_slow = __syncthreads_or(slow);  // also the end of phase a
-    TL(b, 2);
 
     int64_t zeros = 0;
     uint64_t base = 0;
@@ -1293,18 +1243,11 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         //      into the compact staging.  The staging lies in the plan-entry arrays, dead once
         //      phase a is done (n1 + n2 + ka hold 12 bytes per incidence slot, a staged entry
         //      is 12 bytes), so the records' values stay intact for the unstaged fallback.
-#ifdef FA_ROWS_RESORT
-        // the sorted keys are rebuilt from the plan entries (still intact) instead of being
-        // held in registers across phase a
-        if (fast) row_keys(R, start, deg, sk);
-#endif
         const bool staged = !any_slow && total <= CAP;
         double* sv = reinterpret_cast<double*>(R.n1);    // [CAP], spans n1 and n2
         int32_t* sc = reinterpret_cast<int32_t*>(R.ka);  // [CAP]
         if (staged && fast) zeros = walk_row<KIND, false>(R, sk, start, deg, vv, dpos, sc + excl, sv + excl, 0);
-        TL(b, 3);
         base = lookback_wait(A.status, b, uint64_t(total), &s_prefix);  // ends with a barrier
-        TL(b, 4);
         if (active) st_stream_i64(A.rowptr + r, int64_t(base) + excl, pol_first);
         if (active && r == A.nrows - 1) {
             A.rowptr[A.nrows] = int64_t(base) + excl + count;
@@ -1397,7 +1340,6 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         excl = block_exclusive_scan_1b<NT>(count, s_warp, total);
         lookback_publish(A.status, b, uint64_t(total));
     }
-    TL(b, 3);
     // ---- d) merged rows into the compact staging (records are dead), look-back (normally
     //         already resolved), coalesced copy at the symbolic offset
     const bool staged = !__syncthreads_or(slow) && total <= TR::STAGE;
@@ -1432,7 +1374,6 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         }
     }
     base = lookback_wait(A.status, b, uint64_t(total), &s_prefix);  // ends with a barrier
-    TL(b, 4);
     if (active) st_stream_i64(A.rowptr + r, int64_t(base) + excl, pol_first);
     if (active && r == A.nrows - 1) {
         A.rowptr[A.nrows] = int64_t(base) + excl + count;
@@ -1508,7 +1449,6 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
             if (EARLY) atomicAdd(reinterpret_cast<unsigned long long*>(&A.res->reserved[0]), (unsigned long long)bz);
         }
     }
-    TL(b, 5);
 }
 
 // Removes the exactly-zero sums (sparse.py:177-179) in place; exits at once when there are
@@ -1673,10 +1613,7 @@ __device__ __forceinline__ void tri_wt_store(double4* Wt, int64_t k, double ar, 
                  : "memory");
 }
 
-#ifndef FA_TRI_WT_U
-#define FA_TRI_WT_U 4
-#endif
-constexpr int TRI_WT_U = FA_TRI_WT_U;  // triangles in flight per thread
+constexpr int TRI_WT_U = 4;  // triangles in flight per thread
 __global__ void __launch_bounds__(256) k_tri_wt(const int32_t* __restrict__ me, int64_t nme, int64_t nq,
                                                  const double* __restrict__ areas, const double* __restrict__ w,
                                                  double4* __restrict__ Wt, int64_t v0, int64_t v1) {
@@ -1848,10 +1785,13 @@ extern "C" int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t ro
     p->nparts_c = int((nv + (int64_t(1) << p->plog_c) - 1) >> p->plog_c);
     if (p->nparts_c < 1) p->nparts_c = 1;
     p->fine_hist = p->two_level;
-    p->fine_global = p->two_level && p->nparts > FINE_HIST_MAX;
+    p->fine_global = p->two_level && (p->nparts > FINE_HIST_MAX || p->nparts_c > SPLIT_COARSE);
     if (const char* env = getenv("FEMASM_B200_FINE_GLOBAL"))  // test hook: global fine counts
         if (atoi(env) == 1 && p->two_level) p->fine_global = true;
-    p->chunk_place = (nme + PLACE_BLOCKS_PER_SM * NUM_SMS_B200 - 1) / (PLACE_BLOCKS_PER_SM * NUM_SMS_B200);
+    int place_blocks = PLACE_BLOCKS_PER_SM * num_sms();
+    if (const char* env = getenv("FEMASM_B200_PLACE_BLOCKS"))  // test hook: fewer histogram/placement blocks
+        if (atoi(env) >= 1) place_blocks = atoi(env);
+    p->chunk_place = (nme + place_blocks - 1) / place_blocks;
     p->nblk_place = int((nme + p->chunk_place - 1) / p->chunk_place);
     p->ninc = -1;
     const size_t ninc_max = size_t(3) * size_t(nme);
@@ -1913,7 +1853,7 @@ static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* s
     p->ninc = -1;
     p->built = true;
     if (p->nb == 0) {
-        k_reset_result<<<1, 32, 0, st>>>(d_res);
+        k_result_reset<<<1, 32, 0, st>>>(d_res);
         return FA_OK;
     }
     p->me = d_me;
@@ -1938,7 +1878,7 @@ static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* s
         if (!p->Wt) FA_CUDA(cudaMalloc(&p->Wt, sizeof(double4) * size_t(p->nme)));
         P.Wt = p->Wt;
     }
-    const size_t hist_smem = sizeof(unsigned) * (P.fine_hist && !P.fine_global ? p->nparts : p->nparts_c);
+    const size_t hist_smem = sizeof(unsigned) * (P.fine_hist && !P.fine_global ? (p->nparts + 1) / 2 : p->nparts_c);
     FA_CUDA(cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_smem)));
     FA_CUDA(launch_pdl(pdl ? 1 : -1, k_part_hist, dim3(p->nblk_place), dim3(PLACE_THREADS), hist_smem, st, P));
     FA_CUDA(launch_pdl(pdl ? 2 : -1, k_part_scan, dim3(1), dim3(PLAN_THREADS), 0, st, P));
@@ -1965,12 +1905,6 @@ static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* s
     return FA_OK;
 }
 
-#ifdef FA_EXP_TIMELINE
-extern "C" int fa_debug_timeline(void* host_out, int64_t n) {
-    FA_CUDA(cudaMemcpyFromSymbol(host_out, g_tl, sizeof(unsigned long long) * (n < 16384 * 6 ? n : 16384 * 6)));
-    return FA_OK;
-}
-#endif
 
 extern "C" int fa_set_kernel_timer(void* ev_begin, void* ev_end) {
     g_timer_begin = reinterpret_cast<cudaEvent_t>(ev_begin);
@@ -2024,7 +1958,7 @@ extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double
     cudaStream_t st = as_stream(stream);
     const int64_t nrows = fa_plan_rows(p, kind);
     if (nrows == 0 || p->nb == 0) {
-        k_reset_result<<<1, 32, 0, st>>>(d_res);
+        k_result_reset<<<1, 32, 0, st>>>(d_res);
         FA_CUDA(cudaMemsetAsync(d_rowptr, 0, sizeof(int64_t), st));
         return FA_OK;
     }
@@ -2064,7 +1998,8 @@ extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double
     const int64_t rpb = int64_t(BV) * (kind == FA_KIND_ELASTIC ? 2 : 1);
     const size_t cmp_smem = size_t(CMP_CAP) * (sizeof(double) + sizeof(int32_t));
     FA_CUDA(cudaFuncSetAttribute(k_compact, cudaFuncAttributeMaxDynamicSharedMemorySize, int(cmp_smem)));
-    const unsigned cgrid = unsigned(p->nb < 2 * NUM_SMS_B200 ? p->nb : 2 * NUM_SMS_B200);
+    const int64_t cmax = 2 * int64_t(num_sms());
+    const unsigned cgrid = unsigned(p->nb < cmax ? p->nb : cmax);
     FA_CUDA(launch_pdl(8, k_compact, dim3(cgrid), dim3(CMP_THREADS), cmp_smem, st, p->bsym, p->blen, p->bdrop, p->bshift,
                        p->read_done, reinterpret_cast<unsigned long long*>(p->status + p->nb + 1), int64_t(p->nb), rpb,
                        nrows, d_rowptr, d_col, d_val, d_res, reinterpret_cast<unsigned*>(p->status + p->nb + 2)));
@@ -2088,4 +2023,16 @@ extern "C" int fa_assemble_cold(fa_plan* p, const int32_t* d_me, int kind, const
         p->wt_ready = true;
     }
     return fa_assemble(p, kind, d_q, d_areas, d_w, lam, mu, d_rowptr, d_col, d_val, capacity, d_result, stream);
+}
+
+// Development diagnostics (not part of include/femasm_b200.h): copies a plan array to the host
+// after synchronising the device.  what: 0 fine part offsets (nparts + 1), 1 placement part
+// offsets (nparts_c + 1), 2 count matrix (nblk_place x nparts_c).
+extern "C" int fa_plan_debug(fa_plan* p, int what, void* host_out, int64_t n) {
+    if (!p || !host_out) return FA_ERR_ARGUMENT;
+    FA_CUDA(cudaDeviceSynchronize());
+    const unsigned* src = what == 0 ? p->part_off : what == 1 ? p->part_off_c : p->M;
+    const int64_t avail = what == 0 ? p->nparts + 1 : what == 1 ? p->nparts_c + 1 : int64_t(p->nblk_place) * p->nparts_c;
+    FA_CUDA(cudaMemcpy(host_out, src, sizeof(unsigned) * size_t(n < avail ? n : avail), cudaMemcpyDeviceToHost));
+    return FA_OK;
 }

@@ -11,19 +11,6 @@
 
 namespace fa {
 
-__global__ void k_reset_result_b(fa_result* r) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        r->nnz = 0;
-        r->degenerate_index = INT64_MAX;
-        r->index_error_pos = INT64_MAX;
-        r->col_error_pos = INT64_MAX;
-        r->dropped = 0;
-        r->heavy_rows = 0;
-        r->reserved[0] = 0;
-        r->repeat_error_pos = INT64_MAX;
-    }
-}
-
 template <int KIND>
 __global__ void k_element_kg(const int32_t* __restrict__ me, int64_t nme, const double2* __restrict__ q,
                              const double* __restrict__ areas, const double* __restrict__ w, double lam, double mu,
@@ -56,6 +43,43 @@ __global__ void k_element_kg(const int32_t* __restrict__ me, int64_t nme, const 
 #pragma unroll
             for (int r = 0; r < 36; ++r) kg[r * nme + k] = elastic_entry(t, r % 6, r / 6, lam, mu, P);
         }
+    }
+}
+
+// Element-loop strategies (assembly.py:359-397): every triangle's element matrix from the
+// per-element formulas of elements.py, as triplets in triangle-major order (position k*r + il,
+// il = a + order*b, the ravel(order="F") of _assemble_triplet_loop, assembly.py:377-397).
+template <int KIND>
+__global__ void k_element_triplets(const int32_t* __restrict__ me, int64_t nme, const double2* __restrict__ q,
+                                   const double* __restrict__ areas, const double* __restrict__ w, double lam,
+                                   double mu, int64_t* __restrict__ rows, int64_t* __restrict__ cols,
+                                   double* __restrict__ vals, fa_result* res) {
+    constexpr int ORD = KIND == FA_KIND_ELASTIC ? 6 : 3;
+    constexpr int R = ORD * ORD;
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nme; k += int64_t(gridDim.x) * blockDim.x) {
+        const double area = areas[k];
+        if (!(area > AREA_EPS)) atomic_min_i64(&res->degenerate_index, k);  // _check_area (elements.py:27-31)
+        const int c[3] = {me[3 * k], me[3 * k + 1], me[3 * k + 2]};
+        const bool need_q = KIND == FA_KIND_STIFF || KIND == FA_KIND_ELASTIC;
+        const double2 p1 = need_q ? q[c[0]] : make_double2(0.0, 0.0);
+        const double2 p2 = need_q ? q[c[1]] : make_double2(0.0, 0.0);
+        const double2 p3 = need_q ? q[c[2]] : make_double2(0.0, 0.0);
+        const bool need_w = KIND == FA_KIND_MASSW;
+        ElemLoopTri m;
+        elem_loop_matrix<KIND>(p1, p2, p3, area, need_w ? w[c[0]] : 0.0, need_w ? w[c[1]] : 0.0,
+                               need_w ? w[c[2]] : 0.0, lam, mu, m);
+        int64_t ids[ORD];
+#pragma unroll
+        for (int i = 0; i < ORD; ++i) ids[i] = ORD == 3 ? int64_t(c[i]) : 2 * int64_t(c[i / 2]) + (i & 1);
+#pragma unroll
+        for (int b = 0; b < ORD; ++b)
+#pragma unroll
+            for (int a = 0; a < ORD; ++a) {
+                const int64_t o = k * R + a + ORD * b;
+                rows[o] = ids[a];
+                cols[o] = ids[b];
+                vals[o] = m.e[a][b];
+            }
     }
 }
 
@@ -115,7 +139,7 @@ extern "C" int fa_element_kg(int kind, const int32_t* d_me, int64_t nme, const d
     if ((kind == FA_KIND_STIFF || kind == FA_KIND_ELASTIC) && !d_q) { set_error("fa_element_kg: coordinates required"); return FA_ERR_ARGUMENT; }
     if (kind == FA_KIND_MASSW && !d_w) { set_error("WEIGHTED_MASS requires a WeightField"); return FA_ERR_ARGUMENT; }
     cudaStream_t st = as_stream(stream);
-    k_reset_result_b<<<1, 32, 0, st>>>(d_res);
+    k_result_reset<<<1, 32, 0, st>>>(d_res);
     if (nme == 0) return FA_OK;
     const int tb = 256, gb = grid_for(nme, tb);
     const double2* q = reinterpret_cast<const double2*>(d_q);
@@ -126,6 +150,30 @@ extern "C" int fa_element_kg(int kind, const int32_t* d_me, int64_t nme, const d
         default: k_element_kg<FA_KIND_ELASTIC><<<gb, tb, 0, st>>>(d_me, nme, q, d_areas, d_w, lam, mu, d_kg, d_res); break;
     }
     FA_LAUNCH_CHECK("k_element_kg");
+    return FA_OK;
+}
+
+extern "C" int fa_element_triplets(int kind, const int32_t* d_me, int64_t nme, const double* d_q, const double* d_areas,
+                                   const double* d_w, double lam, double mu, int64_t* d_rows, int64_t* d_cols,
+                                   double* d_vals, fa_result* d_res, void* stream) {
+    if (kind < 0 || kind > 3) { set_error("unknown matrix kind %d", kind); return FA_ERR_ARGUMENT; }
+    if (nme < 0 || !d_me || !d_areas || !d_rows || !d_cols || !d_vals || !d_res) {
+        set_error("fa_element_triplets: bad argument"); return FA_ERR_ARGUMENT;
+    }
+    if ((kind == FA_KIND_STIFF || kind == FA_KIND_ELASTIC) && !d_q) { set_error("fa_element_triplets: coordinates required"); return FA_ERR_ARGUMENT; }
+    if (kind == FA_KIND_MASSW && !d_w) { set_error("WEIGHTED_MASS requires a WeightField"); return FA_ERR_ARGUMENT; }
+    cudaStream_t st = as_stream(stream);
+    k_result_reset<<<1, 32, 0, st>>>(d_res);
+    if (nme == 0) return FA_OK;
+    const int tb = 128, gb = grid_for(nme, tb);
+    const double2* q = reinterpret_cast<const double2*>(d_q);
+    switch (kind) {
+        case FA_KIND_MASS: k_element_triplets<FA_KIND_MASS><<<gb, tb, 0, st>>>(d_me, nme, q, d_areas, d_w, lam, mu, d_rows, d_cols, d_vals, d_res); break;
+        case FA_KIND_MASSW: k_element_triplets<FA_KIND_MASSW><<<gb, tb, 0, st>>>(d_me, nme, q, d_areas, d_w, lam, mu, d_rows, d_cols, d_vals, d_res); break;
+        case FA_KIND_STIFF: k_element_triplets<FA_KIND_STIFF><<<gb, tb, 0, st>>>(d_me, nme, q, d_areas, d_w, lam, mu, d_rows, d_cols, d_vals, d_res); break;
+        default: k_element_triplets<FA_KIND_ELASTIC><<<gb, tb, 0, st>>>(d_me, nme, q, d_areas, d_w, lam, mu, d_rows, d_cols, d_vals, d_res); break;
+    }
+    FA_LAUNCH_CHECK("k_element_triplets");
     return FA_OK;
 }
 
@@ -142,7 +190,7 @@ extern "C" int fa_batch_gradients(const int32_t* d_me, int64_t nme, const double
                                   double* d_g, fa_result* d_res, void* stream) {
     if (nme < 0 || !d_me || !d_q || !d_areas || !d_g || !d_res) { set_error("fa_batch_gradients: bad argument"); return FA_ERR_ARGUMENT; }
     cudaStream_t st = as_stream(stream);
-    k_reset_result_b<<<1, 32, 0, st>>>(d_res);
+    k_result_reset<<<1, 32, 0, st>>>(d_res);
     if (nme == 0) return FA_OK;
     const int tb = 256;
     k_gradients<<<grid_for(nme, tb), tb, 0, st>>>(d_me, nme, reinterpret_cast<const double2*>(d_q), d_areas, d_g, d_res);
@@ -154,7 +202,7 @@ extern "C" int fa_compute_areas(const int32_t* d_me, int64_t nme, const double* 
                                 void* stream) {
     if (nme < 0 || !d_me || !d_q || !d_areas || !d_res) { set_error("fa_compute_areas: bad argument"); return FA_ERR_ARGUMENT; }
     cudaStream_t st = as_stream(stream);
-    k_reset_result_b<<<1, 32, 0, st>>>(d_res);
+    k_result_reset<<<1, 32, 0, st>>>(d_res);
     if (nme == 0) return FA_OK;
     const int tb = 256;
     k_areas<<<grid_for(nme, tb), tb, 0, st>>>(d_me, nme, reinterpret_cast<const double2*>(d_q), d_areas, d_res);

@@ -24,6 +24,20 @@ int pdl_mask() {
     return mask;
 }
 
+int num_sms() {
+    // per device (cached): grids are sized in multiples of the SM count
+    static thread_local int cached_dev = -1, cached_n = 0;
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess) return 148;
+    if (dev != cached_dev) {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n < 1) n = 148;
+        cached_dev = dev;
+        cached_n = n;
+    }
+    return cached_n;
+}
+
 int cuda_status(cudaError_t e, const char* what) {
     set_error("%s: %s (%s)", what, cudaGetErrorName(e), cudaGetErrorString(e));
     return FA_ERR_CUDA;

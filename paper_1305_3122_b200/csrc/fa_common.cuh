@@ -1,6 +1,7 @@
 // Shared device/host helpers for the femasm_b200 library (sm_100a).
 #pragma once
 
+#include <climits>
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
@@ -10,7 +11,9 @@
 namespace fa {
 
 constexpr double AREA_EPS = 1e-300;  // mesh.py:27 (AREA_EPS)
-constexpr int NUM_SMS_B200 = 148;
+
+// SM count of the current device (queried once per device; 148 on B200)
+int num_sms();
 
 // ---- host-side error state -------------------------------------------------------------
 void set_error(const char* fmt, ...);
@@ -32,13 +35,16 @@ inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s
 
 // ---- programmatic dependent launch ----------------------------------------------------
 // The kernels of one assembly run back to back on a stream.  Each is launched with
-// programmatic stream serialization and starts with pdl_enter(): it lets the next kernel's
-// blocks be scheduled as soon as all of its own blocks have started (they occupy the SMs this
-// grid's tail leaves idle), then waits until the previous grid has completed and its memory is
-// visible.  Nothing is read or written before the wait, so stream order semantics are kept.
+// programmatic stream serialization and starts with pdl_enter(): it waits until the previous
+// grid has completed and its memory is visible, then lets the next kernel's blocks be
+// scheduled (they occupy the SMs this grid's tail leaves idle and wait in turn).  Nothing is
+// read or written before the wait, so stream order semantics are kept.  The wait comes FIRST:
+// signalling dependents before waiting let a chain of three early-launched kernels (scan ->
+// place -> split) read a plan array before its producer finished (measured: a wrong plan on a
+// small two-level mesh, tests/test_gpu_parity.py::test_fine_histogram_counter_wrap).
 __device__ __forceinline__ void pdl_enter() {
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
 }
 
 // Launch sites that use PDL, one bit per site (0 plan reset, 1 hist, 2 scan, 3 place, 4 split,
@@ -66,7 +72,7 @@ inline cudaError_t launch_pdl(int site, void (*kern)(KArgs...), dim3 grid, dim3 
 
 inline int grid_for(int64_t n, int block, int per_sm = 8) {
     int64_t want = (n + block - 1) / block;
-    int64_t cap = int64_t(NUM_SMS_B200) * per_sm;
+    int64_t cap = int64_t(num_sms()) * per_sm;
     if (want > cap) want = cap;
     if (want < 1) want = 1;
     return int(want);
@@ -75,6 +81,23 @@ inline int grid_for(int64_t n, int block, int per_sm = 8) {
 // ---- device helpers ----------------------------------------------------------------------
 __device__ __forceinline__ void atomic_min_i64(int64_t* addr, int64_t v) {
     atomicMin(reinterpret_cast<long long*>(addr), static_cast<long long>(v));
+}
+
+// fa_result defaults: counters 0, first-offending indices "unset" (INT64_MAX).
+__device__ __forceinline__ void reset_result_fields(fa_result* r) {
+    r->nnz = 0;
+    r->degenerate_index = INT64_MAX;
+    r->index_error_pos = INT64_MAX;
+    r->col_error_pos = INT64_MAX;
+    r->dropped = 0;
+    r->heavy_rows = 0;
+    r->reserved[0] = 0;
+    r->repeat_error_pos = INT64_MAX;
+}
+
+// One-thread reset of a result block (each translation unit gets its own copy of this kernel).
+static __global__ void k_result_reset(fa_result* r) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) reset_result_fields(r);
 }
 
 __device__ __forceinline__ uint64_t ld_volatile_u64(const uint64_t* p) {
@@ -96,6 +119,13 @@ __device__ __forceinline__ uint64_t l2_evict_first_policy() {
 __device__ __forceinline__ unsigned ld_stream_u32(const unsigned* p, uint64_t pol) {
     unsigned v;
     asm volatile("ld.global.L1::no_allocate.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ uint4 ld_stream_u32x4(const uint4* p, uint64_t pol) {
+    uint4 v;
+    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+                 : "l"(p), "l"(pol));
     return v;
 }
 __device__ __forceinline__ int ld_stream_i32(const int* p, uint64_t pol) {
@@ -151,13 +181,6 @@ __device__ __forceinline__ double2 ld_keep_f64x2(const double2* p, uint64_t pol)
     return v;
 }
 
-// Drop a dead 128-byte line from L2 without writing it back (its contents become undefined).
-// Used on intermediate plan arrays once consumed, so their dirty lines neither occupy L2
-// nor cost DRAM write bandwidth.
-__device__ __forceinline__ void l2_discard_line(const void* p) {
-    asm volatile("discard.global.L2 [%0], 128;" ::"l"(p) : "memory");
-}
-
 template <typename T>
 __device__ __forceinline__ T warp_inclusive_scan(T v) {
     const int lane = threadIdx.x & 31;
@@ -176,12 +199,10 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
-// Block-wide exclusive scan of one value per thread.  Returns the exclusive prefix of the
-// calling thread; *total receives the block aggregate.  `warp_tot` is shared scratch of
-// BLOCK/32 entries.
-// Same for small blocks (<= 8 warps) with one barrier: every thread adds up the totals of the
-// warps before its own.  `total` receives the block aggregate in every thread.  Consecutive
-// calls on the same `warp_tot` must be separated by a barrier.
+// Block-wide exclusive scan of one value per thread for small blocks (<= 8 warps) with one
+// barrier: every thread adds up the totals of the warps before its own.  Returns the exclusive
+// prefix of the calling thread; `total` receives the block aggregate in every thread.
+// Consecutive calls on the same `warp_tot` must be separated by a barrier.
 template <int BLOCK, typename T>
 __device__ __forceinline__ T block_exclusive_scan_1b(T v, T* warp_tot, T& total) {
     constexpr int NW = BLOCK / 32;
@@ -201,6 +222,9 @@ __device__ __forceinline__ T block_exclusive_scan_1b(T v, T* warp_tot, T& total)
     return before + inc - v;
 }
 
+// Block-wide exclusive scan of one value per thread.  Returns the exclusive prefix of the
+// calling thread; *total receives the block aggregate.  `warp_tot` is shared scratch of
+// BLOCK/32 entries.
 template <int BLOCK, typename T>
 __device__ __forceinline__ T block_exclusive_scan(T v, T* warp_tot, T* total) {
     constexpr int NW = BLOCK / 32;

@@ -131,4 +131,29 @@ __device__ __forceinline__ double ddiv(double x, double y) {
     return __longlong_as_double(__double_as_longlong(q) | sign);
 }
 
+// Several quotients x_i / y with one divisor (the stiffness row's three entries share 4*area):
+// r = RN(1/y) once (a full correctly rounded division), then each quotient by ddiv_rcp's two
+// residual corrections (Markstein: faithful q + RN(1/y) give RN(x/y)).  Operands, 1/y or the
+// quotient outside the safe exponent range take ddiv for that quotient.
+struct DivBy {
+    double y, r;
+    int ey;
+    bool ok;
+};
+__device__ __forceinline__ DivBy div_prepare(double y) {
+    DivBy d;
+    d.y = y;
+    d.ey = int((__double_as_longlong(y) >> 52) & 0x7ff) - 1023;
+    d.ok = d.ey >= -960 && d.ey <= 960;
+    d.r = d.ok ? ddiv(1.0, y) : 0.0;
+    return d;
+}
+__device__ __forceinline__ double div_by(const DivBy& d, double x) {
+    const int ex = int((__double_as_longlong(x) >> 52) & 0x7ff) - 1023;
+    if (!(d.ok && ex >= -960 && ex <= 960 && ex - d.ey >= -960 && ex - d.ey <= 960)) return ddiv(x, d.y);
+    double q = __dmul_rn(x, d.r);
+    q = __fma_rn(__fma_rn(-q, d.y, x), d.r, q);
+    return __fma_rn(__fma_rn(-q, d.y, x), d.r, q);
+}
+
 }  // namespace fa

@@ -43,6 +43,21 @@ __global__ void k_selftest_div(int64_t n, uint64_t seed, unsigned long long* bad
                 first[0] = x; first[1] = y; first[2] = mine; first[3] = ref;
             }
         }
+        // shared divisor (RN(1/y) once, then residual corrections): the stiffness entries
+        {
+            const DivBy d = div_prepare(y);
+            const double x2 = gen_operand(splitmix64(h + 29));
+            const double xs[2] = {x, x2};
+#pragma unroll
+            for (int j = 0; j < 2; ++j) {
+                const double m3 = div_by(d, xs[j]), r3 = __ddiv_rn(xs[j], y);
+                if (!(m3 != m3 && r3 != r3) && __double_as_longlong(m3) != __double_as_longlong(r3)) {
+                    if (atomicAdd(bad, 1ull) == 0) {
+                        first[0] = xs[j]; first[1] = y; first[2] = m3; first[3] = r3;
+                    }
+                }
+            }
+        }
         // constant divisors of the mass formulas (x only: y fixed)
         const double ys[3] = {6.0, 12.0, 30.0}, rs[3] = {FA_RCP6_, FA_RCP12_, FA_RCP30_};
 #pragma unroll

@@ -60,19 +60,6 @@ static size_t carve(TripletWs* w, void* base, int64_t len) {
     return off;
 }
 
-__global__ void k_trip_reset(fa_result* r) {
-    if (threadIdx.x == 0 && blockIdx.x == 0) {
-        r->nnz = 0;
-        r->degenerate_index = INT64_MAX;
-        r->index_error_pos = INT64_MAX;
-        r->col_error_pos = INT64_MAX;
-        r->dropped = 0;
-        r->heavy_rows = 0;
-        r->reserved[0] = 0;
-        r->repeat_error_pos = INT64_MAX;
-    }
-}
-
 __global__ void k_trip_keys(const int64_t* __restrict__ rows, const int64_t* __restrict__ cols, int64_t len,
                             int64_t n_rows, int64_t n_cols, uint64_t* __restrict__ key, int64_t* __restrict__ idx,
                             fa_result* res) {
@@ -183,20 +170,23 @@ __global__ void k_trip_heads(const uint64_t* __restrict__ key, int64_t len, int*
 
 // One thread per run of equal keys: left-to-right sum in input order (the stable sort kept
 // ties in input order), then flag the position when the sum is nonzero.
+// keep_zeros (CscBuilder semantics, sparse.py:208-290): the sum starts from the run's first
+// value (`aa[pos] += v` after the first insertion stores v) and every position is stored.
 __global__ void k_trip_sums(const uint64_t* __restrict__ key, const int64_t* __restrict__ idx,
                             const double* __restrict__ vals, int64_t len, int* __restrict__ keep,
-                            double* __restrict__ sums, fa_result* res) {
+                            double* __restrict__ sums, fa_result* res, int keep_zeros) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < len; i += int64_t(gridDim.x) * blockDim.x) {
         const bool head = i == 0 || key[i] != key[i - 1];
         if (!head) { keep[i] = 0; continue; }
-        double s = 0.0;
-        int64_t j = i;
-        do {
+        double s = keep_zeros ? vals[idx[i]] : 0.0;
+        int64_t j = keep_zeros ? i + 1 : i;
+        while (j < len && key[j] == key[i]) {
             s = __dadd_rn(s, vals[idx[j]]);
             ++j;
-        } while (j < len && key[j] == key[i]);
+        }
         sums[i] = s;
-        keep[i] = s != 0.0 ? 1 : 0;
+        keep[i] = (s != 0.0 || keep_zeros) ? 1 : 0;
+        if (keep_zeros) continue;
         if (s == 0.0) {
             // count only positions with at least one nonzero input (the reference never sees
             // all-zero positions); diagnostic only
@@ -250,9 +240,20 @@ extern "C" size_t fa_triplets_workspace(int64_t len, int64_t n_rows, int64_t n_c
 
 static int scan_i32_flags(const int* flag, int64_t* pos, int64_t n, TripletWs& w, cudaStream_t st);
 
+extern "C" int fa_triplets_to_csc_ex(const int64_t* d_rows, const int64_t* d_cols, const double* d_vals, int64_t len,
+                                     int64_t n_rows, int64_t n_cols, int flags, int64_t* d_colptr, int64_t* d_rowidx,
+                                     double* d_vals_out, void* d_ws, size_t ws_bytes, fa_result* d_res, void* stream);
+
 extern "C" int fa_triplets_to_csc(const int64_t* d_rows, const int64_t* d_cols, const double* d_vals, int64_t len,
                                   int64_t n_rows, int64_t n_cols, int64_t* d_colptr, int64_t* d_rowidx,
                                   double* d_vals_out, void* d_ws, size_t ws_bytes, fa_result* d_res, void* stream) {
+    return fa_triplets_to_csc_ex(d_rows, d_cols, d_vals, len, n_rows, n_cols, 0, d_colptr, d_rowidx, d_vals_out, d_ws,
+                                 ws_bytes, d_res, stream);
+}
+
+extern "C" int fa_triplets_to_csc_ex(const int64_t* d_rows, const int64_t* d_cols, const double* d_vals, int64_t len,
+                                     int64_t n_rows, int64_t n_cols, int flags, int64_t* d_colptr, int64_t* d_rowidx,
+                                     double* d_vals_out, void* d_ws, size_t ws_bytes, fa_result* d_res, void* stream) {
     if (len < 0 || n_rows < 1 || n_cols < 1) { set_error("matrix dimensions must be positive"); return FA_ERR_ARGUMENT; }
     if (!d_colptr || !d_res || !d_ws || (len > 0 && (!d_rows || !d_cols || !d_vals || !d_rowidx || !d_vals_out))) {
         set_error("fa_triplets_to_csc: NULL argument"); return FA_ERR_ARGUMENT;
@@ -262,7 +263,7 @@ extern "C" int fa_triplets_to_csc(const int64_t* d_rows, const int64_t* d_cols, 
     TripletWs w;
     void* base = reinterpret_cast<void*>((reinterpret_cast<uintptr_t>(d_ws) + 255) & ~uintptr_t(255));
     carve(&w, base, len);
-    k_trip_reset<<<1, 32, 0, st>>>(d_res);
+    k_result_reset<<<1, 32, 0, st>>>(d_res);
     if (len == 0) {
         FA_CUDA(cudaMemsetAsync(d_colptr, 0, sizeof(int64_t) * (n_cols + 1), st));
         return FA_OK;
@@ -292,7 +293,8 @@ extern "C" int fa_triplets_to_csc(const int64_t* d_rows, const int64_t* d_cols, 
     }
     // sums per run (values gathered through the permutation); reuse kout as f64 storage
     double* sums = reinterpret_cast<double*>(kout);
-    k_trip_sums<<<grid_for(len, tb), tb, 0, st>>>(kin, iin, d_vals, len, w.flag, sums, d_res);
+    k_trip_sums<<<grid_for(len, tb), tb, 0, st>>>(kin, iin, d_vals, len, w.flag, sums, d_res,
+                                                   (flags & FA_TRIPLETS_KEEP_ZEROS) ? 1 : 0);
     FA_LAUNCH_CHECK("k_trip_sums");
     int rc = scan_i32_flags(w.flag, w.pos, len, w, st);
     if (rc != FA_OK) return rc;

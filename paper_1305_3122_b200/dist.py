@@ -110,8 +110,16 @@ class DistributedAssembler:
         """Plan build + fused assembly of this rank's rows; with `exchange`, the NCCL
         allgather of local nnz gives the global entry offset.  Returns (rowptr, col, val,
         entry_offset, total_nnz, fa_result)."""
+        from . import _lib
+        from .mesh import DegenerateTriangleError
+
         self.plan.build(me_dev)
+        self.plan.check_build()  # out-of-range / repeated vertex ids: the reference's ValueError
         rowptr, col, val, r = self.plan.assemble(self.kind, q=q, areas=areas, w=w, lam=lam, mu=mu)
+        if r.degenerate_index != _lib.INT64_MAX:
+            k = int(r.degenerate_index)
+            area = float(areas[k].item()) if areas is not None else 0.0
+            raise DegenerateTriangleError(k, area)
         offset, total = (0, int(r.nnz))
         if exchange and self.world > 1:
             offset, total = global_offsets(int(r.nnz))

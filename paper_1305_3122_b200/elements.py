@@ -60,6 +60,8 @@ def _check_area(area: float) -> float:
 
 
 def _one_triangle(kind_code: int, pts, area: float, w=None, lam=0.0, mu=0.0) -> np.ndarray:
+    """One element matrix with the per-element formulas of elements.py (fa_element_triplets:
+    the arithmetic of the element-loop strategies, not the batch kernels')."""
     import torch
 
     from . import _lib
@@ -71,14 +73,16 @@ def _one_triangle(kind_code: int, pts, area: float, w=None, lam=0.0, mu=0.0) -> 
     me = torch.tensor([[0, 1, 2]], dtype=torch.int32, device=dev)
     areas = torch.tensor([area], dtype=torch.float64, device=dev)
     wd = torch.tensor(np.asarray(w, dtype=np.float64), device=dev) if w is not None else None
-    r = 36 if kind_code == 3 else 9
-    kg = torch.empty((r, 1), dtype=torch.float64, device=dev)
-    res = ResultBlock()
-    rc = _lib.lib().fa_element_kg(kind_code, me.data_ptr(), 1, q.data_ptr(), areas.data_ptr(), _lib.ptr(wd),
-                                  float(lam), float(mu), kg.data_ptr(), res.ptr, _lib.stream_handle())
-    _lib.check(rc, "fa_element_kg")
     order = 6 if kind_code == 3 else 3
-    return kg.cpu().numpy()[:, 0].reshape(order, order, order="F").copy()
+    rows = torch.empty(order * order, dtype=torch.int64, device=dev)
+    cols = torch.empty_like(rows)
+    vals = torch.empty(order * order, dtype=torch.float64, device=dev)
+    res = ResultBlock()
+    rc = _lib.lib().fa_element_triplets(kind_code, me.data_ptr(), 1, q.data_ptr(), areas.data_ptr(), _lib.ptr(wd),
+                                        float(lam), float(mu), rows.data_ptr(), cols.data_ptr(), vals.data_ptr(),
+                                        res.ptr, _lib.stream_handle())
+    _lib.check(rc, "fa_element_triplets")
+    return vals.cpu().numpy().reshape(order, order, order="F").copy()
 
 
 def elem_mass(area: float) -> np.ndarray:

@@ -43,7 +43,11 @@ class AssemblyPlan:
         rc = _lib.lib().fa_plan_build(self._h, me_dev.data_ptr(), self._build_res.ptr, _lib.stream_handle(stream))
         _lib.check(rc, "fa_plan_build")
 
-    def check_build(self) -> None:
+    def check_build(self, stream=None) -> None:
+        """Raise the reference's ValueError for an invalid connectivity (mesh.py:95-103).
+        Synchronises `stream` (the one the build ran on) first."""
+        if stream is not None:
+            stream.synchronize()
         r = self._build_res.fetch()
         if r.index_error_pos != _lib.INT64_MAX:
             raise ValueError("connectivity index out of range [0, nq)")
@@ -95,7 +99,11 @@ class AssemblyPlan:
         val = torch.empty(max(cap, 1), dtype=torch.float64, device=dev)
         res = ResultBlock()
         self.assemble_into(kind, q, areas, w, lam, mu, rowptr, col, val, res, stream)
+        if stream is not None:  # the result block is read on the current stream below
+            stream.synchronize()
         r = res.fetch()  # synchronises
+        if r.nnz > cap:
+            raise RuntimeError(f"assembly produced {r.nnz} entries but the plan's capacity is {cap}")
         return rowptr, col[: r.nnz], val[: r.nnz], r
 
     def close(self) -> None:

@@ -211,7 +211,10 @@ def csc_from_triplets(rows, cols, vals, n_rows: int, n_cols: int) -> CscMatrix:
     return _triplets_device(d_rows, d_cols, d_vals, int(n_rows), int(n_cols), host_rows=rows, host_cols=cols)
 
 
-def _triplets_device(d_rows, d_cols, d_vals, n_rows, n_cols, host_rows=None, host_cols=None) -> CscMatrix:
+def _triplets_device(d_rows, d_cols, d_vals, n_rows, n_cols, host_rows=None, host_cols=None,
+                     keep_zeros: bool = False) -> CscMatrix:
+    """Device triplets -> CscMatrix: Matlab sparse() (sparse.py:140-189), or with `keep_zeros`
+    the CscBuilder semantics of the element-loop strategies (sparse.py:208-290)."""
     torch = require_cuda()
     dev = device()
     n = int(d_vals.numel())
@@ -222,10 +225,10 @@ def _triplets_device(d_rows, d_cols, d_vals, n_rows, n_cols, host_rows=None, hos
     rowidx = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
     vout = torch.empty(max(n, 1), dtype=torch.float64, device=dev)
     res = ResultBlock()
-    rc = L.fa_triplets_to_csc(
+    rc = L.fa_triplets_to_csc_ex(
         _lib.ptr(d_rows) if n else None, _lib.ptr(d_cols) if n else None, _lib.ptr(d_vals) if n else None,
-        n, n_rows, n_cols, colptr.data_ptr(), rowidx.data_ptr(), vout.data_ptr(), ws.data_ptr(), ws_bytes,
-        res.ptr, _lib.stream_handle(),
+        n, n_rows, n_cols, _lib.FA_TRIPLETS_KEEP_ZEROS if keep_zeros else 0, colptr.data_ptr(), rowidx.data_ptr(),
+        vout.data_ptr(), ws.data_ptr(), ws_bytes, res.ptr, _lib.stream_handle(),
     )
     _lib.check(rc, "fa_triplets_to_csc")
     r = res.fetch()

@@ -4,6 +4,8 @@ the committed outputs.
 
     python tests/golden/make_golden.py small           -> tests/golden/small_cases.npz
     python tests/golden/make_golden.py digests C1 C2   -> tests/golden/reference_digests.json
+    python tests/golden/make_golden.py digests C5ALL    -> every C5 row block + the whole C5 digest
+    python tests/golden/make_golden.py loops           -> tests/golden/loop_cases.npz
 
 small_cases.npz: seeded BASELINE-family meshes (tiny N), the reference's own generators
 (square / disk) and the reference's OptV2 output for every kind, as full arrays.
@@ -111,6 +113,50 @@ def small():
             out[f"{name}/{kind}/values"] = m.values
     np.savez_compressed(HERE / "small_cases.npz", **out)
     print("small cases:", cases + list(gens))
+
+
+def loops():
+    """Element-loop strategies (CLASSICAL, OPTV0, OPTV1; assembly.py:359-397) and the
+    per-element API elem_* (elements.py:34-154) of the reference, as full arrays ->
+    tests/golden/loop_cases.npz.  The reference builds CLASSICAL/OPTV0 with CscBuilder
+    (explicit zeros kept) and every strategy with the per-element formulas, so the bits differ
+    from OPTV2's; the meshes are small because the reference's CscBuilder is O(nnz) per
+    insertion."""
+    out = {}
+    rng = np.random.default_rng(7)
+    # elem_*: random triangles (counterclockwise, well shaped), weights, Lame parameters
+    P = rng.uniform(-1.0, 1.0, (64, 3, 2))
+    P[:, 1] = P[:, 0] + rng.uniform(0.2, 1.0, (64, 2)) * [1.0, 0.1]
+    P[:, 2] = P[:, 0] + rng.uniform(0.2, 1.0, (64, 2)) * [0.1, 1.0]
+    A = femasm.compute_areas(P.reshape(-1, 2), np.arange(192).reshape(64, 3))
+    W = rng.uniform(0.5, 2.0, (64, 3))
+    out["elem/P"], out["elem/A"], out["elem/W"] = P, A, W
+    params = femasm.ElasticParams(1.3, 0.4)
+    out["elem/lam_mu"] = np.array([1.3, 0.4])
+    out["elem/mass"] = np.stack([femasm.elem_mass(a) for a in A])
+    out["elem/massw"] = np.stack([femasm.elem_mass_weighted(a, *w) for a, w in zip(A, W)])
+    out["elem/stiff"] = np.stack([femasm.elem_stiff(p[0], p[1], p[2], a) for p, a in zip(P, A)])
+    out["elem/elastic"] = np.stack([femasm.elem_stiff_elastic(p[0], p[1], p[2], a, params) for p, a in zip(P, A)])
+    meshes = {
+        "square_n4": femasm.generate_unit_square_mesh(4),
+        "disk_n4": femasm.generate_disk_mesh(4),
+        "seeded_n5_s1": femasm.Mesh(seeded_square_mesh(5, 1).vertices, seeded_square_mesh(5, 1).connectivity),
+    }
+    for name, mesh in meshes.items():
+        out[f"{name}/V"] = mesh.vertices
+        out[f"{name}/C"] = mesh.connectivity
+        for kind in KIND:
+            kw = {}
+            if kind == "massw":
+                kw["weight"] = femasm.WeightField.quadratic()
+            if kind == "elastic":
+                kw["params"] = femasm.ElasticParams(2.0, 0.7)
+            for strat in ("CLASSICAL", "OPTV0", "OPTV1"):
+                m = femasm.assemble(mesh, KIND[kind], getattr(femasm.Strategy, strat), **kw)
+                for f in ("col_ptr", "row_idx", "values"):
+                    out[f"{name}/{kind}/{strat}/{f}"] = getattr(m, f)
+    np.savez_compressed(HERE / "loop_cases.npz", **out)
+    print("loop cases:", list(meshes))
 
 
 def digests(names):
@@ -258,5 +304,7 @@ def row_block_digest(data, path, cfg, G, blk, seed=0):
 if __name__ == "__main__":
     if sys.argv[1] == "small":
         small()
+    elif sys.argv[1] == "loops":
+        loops()
     elif sys.argv[1] == "digests":
         digests(sys.argv[2:])

@@ -41,3 +41,18 @@ def rel_err(got_vals, ref_vals) -> float:
     ref = np.asarray(ref_vals)
     scale = np.abs(ref).max() if ref.size else 1.0
     return float(np.abs(np.asarray(got_vals) - ref).max() / scale) if ref.size else 0.0
+
+
+def csr_digests_device(rowptr, col, val, chunk=1 << 26):
+    """SHA-256 of device CSR arrays in femasm's CSC dtypes (int64, int64, f64), streamed to the
+    host in chunks (the C5 matrix does not need a second full host copy)."""
+    import torch
+
+    out = []
+    for t, dt in ((rowptr, torch.int64), (col, torch.int64), (val, torch.float64)):
+        h = hashlib.sha256()
+        for s in range(0, t.numel(), chunk):
+            h.update(np.ascontiguousarray(t[s:s + chunk].to(dt).cpu().numpy()).astype(
+                "<i8" if dt is torch.int64 else "<f8", copy=False).tobytes())
+        out.append(h.hexdigest())
+    return tuple(out)

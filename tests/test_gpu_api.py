@@ -124,6 +124,8 @@ def test_csc_from_triplets_long_runs_and_large_keys():
 
 @pytest.mark.parametrize("kind", list(fa.MatrixKind))
 def test_assemble_all_strategies_match_reference(golden, kind):
+    """OPTV2 is bitwise the reference's OPTV2; the element-loop strategies agree with it to
+    roundoff (the reference's own contract, test_acceptance.py:87-106)."""
     name = "seeded_n16_s0"
     mesh = mesh_of(golden, name)
     kw = {}
@@ -132,10 +134,67 @@ def test_assemble_all_strategies_match_reference(golden, kind):
     if kind is fa.MatrixKind.ELASTIC:
         kw["params"] = fa.ElasticParams(*golden[f"{name}/elastic/lam_mu"])
     ref = tuple(golden[f"{name}/{kind.value}/{f}"] for f in ("col_ptr", "row_idx", "values"))
-    for strategy in fa.Strategy:
+    m2 = fa.assemble(mesh, kind, fa.Strategy.OPTV2, **kw)
+    assert_same_csc((m2.col_ptr, m2.row_idx, m2.values), ref, f"{kind}/OPTV2")
+    scale = np.abs(m2.values).max()
+    for strategy in (fa.Strategy.CLASSICAL, fa.Strategy.OPTV0, fa.Strategy.OPTV1):
         m = fa.assemble(mesh, kind, strategy, **kw)
         assert m.shape == (kind.n_dof(mesh.nq),) * 2
-        assert_same_csc((m.col_ptr, m.row_idx, m.values), ref, f"{kind}/{strategy}")
+        assert fa.max_abs_diff(m, m2) <= 1e-12 * scale, f"{kind}/{strategy}"
+
+
+@pytest.fixture(scope="module")
+def loops():
+    from conftest import GOLDEN
+
+    d = np.load(GOLDEN / "loop_cases.npz")
+    return {k: d[k] for k in d.files}
+
+
+@pytest.mark.parametrize("strategy", ["CLASSICAL", "OPTV0", "OPTV1"])
+@pytest.mark.parametrize("kind", ["mass", "massw", "stiff", "elastic"])
+@pytest.mark.parametrize("name", ["square_n4", "disk_n4", "seeded_n5_s1"])
+def test_element_loop_strategies_bitwise(loops, name, kind, strategy):
+    """CLASSICAL / OPTV0 / OPTV1 bitwise against the reference's own element loops
+    (assembly.py:359-397): per-element formulas (elements.py), CscBuilder's explicit zeros for
+    CLASSICAL / OPTV0 (sparse.py:208-290), Matlab sparse() for OPTV1."""
+    mesh = fa.Mesh(loops[f"{name}/V"], loops[f"{name}/C"])
+    kw = {}
+    if kind == "massw":
+        kw["weight"] = fa.WeightField.quadratic()
+    if kind == "elastic":
+        kw["params"] = fa.ElasticParams(2.0, 0.7)
+    m = fa.assemble(mesh, fa.MatrixKind(kind), getattr(fa.Strategy, strategy), **kw)
+    ref = tuple(loops[f"{name}/{kind}/{strategy}/{f}"] for f in ("col_ptr", "row_idx", "values"))
+    assert_same_csc((m.col_ptr, m.row_idx, m.values), ref, f"{name}/{kind}/{strategy}")
+
+
+def test_incremental_keeps_zeros_triplet_drops_them():
+    """test_assembly.py:269-276: on the unit square the stiffness has exact-zero sums; the
+    CscBuilder strategies store them, the triplet strategies drop them."""
+    mesh = fa.generate_unit_square_mesh(4)
+    classical = fa.assemble(mesh, fa.MatrixKind.STIFFNESS, fa.Strategy.CLASSICAL)
+    optv2 = fa.assemble(mesh, fa.MatrixKind.STIFFNESS, fa.Strategy.OPTV2)
+    assert classical.nnz > optv2.nnz
+    assert (classical.values == 0.0).any() and not (optv2.values == 0.0).any()
+    assert fa.max_abs_diff(classical, optv2) <= 1e-14
+
+
+def test_elem_functions_bitwise(loops):
+    """elem_mass / elem_mass_weighted / elem_stiff / elem_stiff_elastic bitwise against the
+    reference's per-element arithmetic (elements.py:34-154) on 64 random triangles."""
+    P, A, W = loops["elem/P"], loops["elem/A"], loops["elem/W"]
+    params = fa.ElasticParams(*loops["elem/lam_mu"])
+    for t in range(len(A)):
+        got = {
+            "mass": fa.elem_mass(A[t]),
+            "massw": fa.elem_mass_weighted(A[t], *W[t]),
+            "stiff": fa.elem_stiff(P[t, 0], P[t, 1], P[t, 2], A[t]),
+            "elastic": fa.elem_stiff_elastic(P[t, 0], P[t, 1], P[t, 2], A[t], params),
+        }
+        for k, g in got.items():
+            ref = loops[f"elem/{k}"][t]
+            assert np.array_equal(g.view(np.int64), ref.view(np.int64)), f"elem {k} triangle {t}"
 
 
 def test_assemble_reference_invariants():

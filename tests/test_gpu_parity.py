@@ -251,6 +251,38 @@ def test_large_part_general_sort_path(monkeypatch, kind, part_log2):
     assert_same_csc(got, ref, f"{kind} part_log2={part_log2}")
 
 
+def hub_part_mesh(n_hubs=1024, spokes=50):
+    """n_hubs small fans (hub degree `spokes`) with the hubs numbered first, so the first fine
+    part (1024 vertices) holds n_hubs * spokes incidences and every 128-hub bucket overflows
+    its shared-memory slots."""
+    Vf, Cf = fan_mesh(spokes, n_rings=1)  # hub 0, ring 1..spokes
+    nv_f = Vf.shape[0]
+    V = np.zeros((n_hubs * nv_f, 2))
+    C = []
+    for h in range(n_hubs):
+        ids = np.concatenate([[h], n_hubs + h * (nv_f - 1) + np.arange(nv_f - 1)])
+        V[ids] = Vf + np.array([h, 0.0]) * 3.0
+        C.append(ids[Cf])
+    C = np.concatenate(C)
+    return V, C[np.random.default_rng(1).permutation(len(C))]
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_fine_histogram_counter_wrap(monkeypatch, kind):
+    """71,680 incidences of one fine part counted by ONE histogram block: its 16-bit shared
+    counter wraps (65536 handed to the global fine count and to the block's coarse count).
+    Two-level plan forced; bitwise against the oracle."""
+    monkeypatch.setenv("FEMASM_B200_COARSE_LOG2", "11")
+    monkeypatch.setenv("FEMASM_B200_PLACE_BLOCKS", "1")
+    V, C = hub_part_mesh(1024, 70)
+    areas = fo.triangle_areas(V, C)
+    w = 0.5 + (np.arange(V.shape[0]) % 7) * 0.25
+    ref = c_oracle.assemble(kind, V, C, areas, w, 2.0, 0.7)
+    got, r = plan_assemble(kind, V, C, areas, w, 2.0, 0.7)
+    assert r.heavy_rows > 0
+    assert_same_csc(got, ref, f"{kind} wrapped fine counter")
+
+
 def test_isolated_vertices_have_empty_rows():
     """A vertex no triangle references has no triplet, hence an empty row (reference)."""
     sm = seeded_square_mesh(8, 1)
@@ -355,3 +387,110 @@ def test_assemble_cold_entry_point(kind, block):
         plan.check_build()
         got = (rowptr.cpu().numpy(), col[: r.nnz].cpu().numpy(), val[: r.nnz].cpu().numpy())
         assert_same_csc(got, ref, f"{kind} cold call {it}")
+
+
+# ------------------------------------------------------------------------------------------
+# the exact timed path of bench.py at BASELINE sizes: fa_assemble_cold from device-resident
+# me/q, areas recomputed in the row kernel (stiffness, elasticity) or computed on the device
+# (mass, weighted mass; the W records then come from the plan's histogram pass)
+# ------------------------------------------------------------------------------------------
+def cold_assemble(kind, sm, lam=1.0, mu=0.5, v0=0, v1=None, hash_only=True):
+    """bench.py's step (fa_assemble_cold) on seeded mesh `sm`; returns the three CSR digests
+    (femasm dtypes) and the fa_result."""
+    import torch
+    from helpers import csr_digests_device
+    from paper_1305_3122_b200.device import ResultBlock
+
+    dev = torch.device("cuda")
+    me = torch.from_numpy(np.ascontiguousarray(sm.connectivity, dtype=np.int32)).to(dev)
+    q = torch.from_numpy(sm.vertices).to(dev)
+    w = torch.from_numpy(sm.weights).to(dev) if kind == "massw" else None
+    a = None
+    if kind in ("mass", "massw"):
+        a = torch.empty(sm.nme, dtype=torch.float64, device=dev)
+        ar = ResultBlock()
+        _lib.check(_lib.lib().fa_compute_areas(me.data_ptr(), sm.nme, q.data_ptr(), a.data_ptr(), ar.ptr,
+                                               _lib.stream_handle()))
+    v1 = sm.nq if v1 is None else v1
+    plan = fa.AssemblyPlan(sm.nme, sm.nq, v0, v1)
+    plan.build(me)
+    cap = plan.capacity(kind)
+    rowptr = torch.empty(plan.rows(kind) + 1, dtype=torch.int64, device=dev)
+    col = torch.empty(cap, dtype=torch.int32, device=dev)
+    val = torch.empty(cap, dtype=torch.float64, device=dev)
+    res = ResultBlock()
+    for _ in range(2):  # twice: the second call reuses the plan's buffers (as the bench's steps)
+        plan.assemble_cold_into(me, kind, q if kind in ("stiff", "elastic") else None, a, w, lam, mu,
+                                rowptr, col, val, res)
+    r = res.fetch()
+    plan.check_build()
+    assert r.nnz <= cap
+    return csr_digests_device(rowptr, col[: r.nnz], val[: r.nnz]), r
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("key", ["C1/s0", "C1/s1", "C1/s2", "C2/s0", "C2/s1", "C2/s2", "C3/s0", "C4/s0", "C4/s1",
+                                 "C4/s2", "EL64/s0"])
+def test_timed_path_digests(digests, key):
+    """bench.py's exact step against femasm's digests at full BASELINE sizes."""
+    d = digests[key]
+    sm = seeded_square_mesh(d["N"], d["seed"])
+    got, r = cold_assemble(d["kind"], sm, d["lam"] if d["lam"] is not None else 1.0,
+                           d["mu"] if d["mu"] is not None else 0.5)
+    assert r.nnz == d["nnz"]
+    assert got == (d["col_ptr_sha256"], d["row_idx_sha256"], d["values_sha256"])
+
+
+@pytest.fixture(scope="module")
+def c5_mesh():
+    return seeded_square_mesh(8192, 0)
+
+
+@pytest.mark.slow
+def test_c5_whole_matrix_digest(digests, c5_mesh):
+    """C5 (134M triangles, 470M entries) on one GPU through bench.py's step, against the digest
+    of femasm's whole C5 matrix (streamed from its row-block subsets, make_golden.py C5ALL)."""
+    d = digests["C5/s0"]
+    got, r = cold_assemble("stiff", c5_mesh)
+    assert r.nnz == d["nnz"]
+    assert got == (d["col_ptr_sha256"], d["row_idx_sha256"], d["values_sha256"])
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("blk", range(8))
+def test_c5_g8_row_blocks(digests, c5_mesh, blk):
+    """Every block of the 8-way row split (the multi-GPU decomposition), cold path, against
+    femasm's row-block subset digests."""
+    d = digests[f"C5B/s0/G8/b{blk}"]
+    got, r = cold_assemble("stiff", c5_mesh, v0=d["v0"], v1=d["v1"])
+    assert r.nnz == d["nnz"]
+    assert got == (d["col_ptr_sha256"], d["row_idx_sha256"], d["values_sha256"])
+
+
+@pytest.mark.parametrize("kind", KINDS)
+def test_reused_plan_with_changed_values(kind):
+    """Warm re-assembly: one plan, new numeric inputs each call -
+    weights, Lame parameters, coordinates (with recomputed areas) - each bitwise against the
+    oracle for those inputs."""
+    import torch
+    from paper_1305_3122_b200.device import ResultBlock
+
+    sm = seeded_square_mesh(40, 6)
+    dev = torch.device("cuda")
+    me = torch.from_numpy(np.ascontiguousarray(sm.connectivity, dtype=np.int32)).to(dev)
+    plan = fa.AssemblyPlan(sm.nme, sm.nq)
+    plan.build(me)
+    rng = np.random.default_rng(11)
+    for it in range(3):
+        V = sm.vertices.copy()
+        interior = (V[:, 0] > 0) & (V[:, 0] < 1) & (V[:, 1] > 0) & (V[:, 1] < 1)
+        V[interior] += rng.uniform(-0.002, 0.002, (int(interior.sum()), 2)) * it
+        w = rng.uniform(0.5, 2.0, sm.nq) if it else sm.weights
+        lam, mu = [(1.0, 0.5), (2.0, 0.7), (0.3, 1.9)][it]
+        areas = fo.triangle_areas(V, sm.connectivity)
+        ref = c_oracle.assemble(kind, V, sm.connectivity, areas, w, lam, mu)
+        q = torch.from_numpy(V).to(dev)
+        a = None if kind in ("stiff", "elastic") else torch.from_numpy(areas).to(dev)
+        wd = torch.from_numpy(w).to(dev)
+        rowptr, col, val, r = plan.assemble(kind, q=q, areas=a, w=wd, lam=lam, mu=mu)
+        assert_same_csc((rowptr.cpu().numpy(), col.cpu().numpy(), val.cpu().numpy()), ref, f"{kind} call {it}")
