@@ -152,6 +152,15 @@ int fa_build_ig_jg(int vector, const int32_t* d_me, int64_t nme, int32_t* d_ig, 
 int fa_batch_gradients(const int32_t* d_me, int64_t nme, const double* d_q, const double* d_areas,
                        double* d_g, fa_result* d_result, void* stream);
 
+/* Mesh construction on the device (femasm Mesh.__init__, mesh.py:84-119 + compute_areas,
+ * mesh.py:51-69) in one pass over the caller's int64 connectivity d_me64 (nme x 3): the first
+ * out-of-range flattened position -> d_result->index_error_pos, the first triangle repeating a
+ * vertex id -> repeat_error_pos, the int32 copy the plans use -> d_me32, areas (bitwise
+ * compute_areas; 0 for a triangle with a bad id) -> d_areas, the first area <= 1e-300 ->
+ * degenerate_index.  The caller raises them in the reference's order (range, repeat, area). */
+int fa_mesh_ingest(const int64_t* d_me64, int64_t nme, int64_t nq, const double* d_q,
+                   int32_t* d_me32, double* d_areas, fa_result* d_result, void* stream);
+
 /* compute_areas (mesh.py:51-69): 0.5*|cross|, first area <= 1e-300 reported. */
 int fa_compute_areas(const int32_t* d_me, int64_t nme, const double* d_q, double* d_areas,
                      fa_result* d_result, void* stream);
@@ -195,6 +204,15 @@ int fa_element_triplets(int kind, const int32_t* d_me, int64_t nme, const double
  * lines in CSC order, values "%.17g".  threads <= 0: all hardware threads.  Host only. */
 int fa_write_matrix_market(const char* path, int64_t n_rows, int64_t n_cols, const int64_t* col_ptr,
                            const int64_t* row_idx, const double* values, int threads);
+
+/* femasm read_mesh (mesh.py:225-286) for well-formed files: header "nq nme", nq lines "x y",
+ * nme lines of 1-based ids.  Host only, multithreaded (threads <= 0: all).  Call with
+ * vertices == connectivity == NULL to read the header into *nq / *nme, then with (nq x 2) f64
+ * and (nme x 3) int64 (0-based ids written) buffers.  FA_ERR_ARGUMENT (no message) when the
+ * file is not in the strict layout write_mesh produces - the caller then parses it with the
+ * reference's rules, which produce the reference's MeshFormatError. */
+int fa_read_mesh_text(const char* path, int64_t* nq, int64_t* nme, double* vertices,
+                      int64_t* connectivity, int threads);
 
 /* ------------------------------------------------------------------------------------
  * Diagnostics.  fa_selftest_division compares the library's call-free correctly rounded

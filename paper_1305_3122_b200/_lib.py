@@ -46,6 +46,7 @@ EXPORTED_SYMBOLS = (
     "fa_build_ig_jg",
     "fa_batch_gradients",
     "fa_compute_areas",
+    "fa_mesh_ingest",
     "fa_triplets_workspace",
     "fa_triplets_to_csc",
     "fa_triplets_to_csc_ex",
@@ -53,6 +54,7 @@ EXPORTED_SYMBOLS = (
     "fa_selftest_division",
     "fa_set_kernel_timer",
     "fa_write_matrix_market",
+    "fa_read_mesh_text",
 )
 
 
@@ -104,6 +106,7 @@ _SIGNATURES = {
     "fa_build_ig_jg": (_I, [_I, _P, _I64, _P, _P, _P]),
     "fa_batch_gradients": (_I, [_P, _I64, _P, _P, _P, _P, _P]),
     "fa_compute_areas": (_I, [_P, _I64, _P, _P, _P, _P]),
+    "fa_mesh_ingest": (_I, [_P, _I64, _I64, _P, _P, _P, _P, _P]),
     "fa_triplets_workspace": (ctypes.c_size_t, [_I64, _I64, _I64]),
     "fa_triplets_to_csc": (_I, [_P, _P, _P, _I64, _I64, _I64, _P, _P, _P, _P, ctypes.c_size_t, _P, _P]),
     "fa_triplets_to_csc_ex": (_I, [_P, _P, _P, _I64, _I64, _I64, _I, _P, _P, _P, _P, ctypes.c_size_t, _P, _P]),
@@ -111,6 +114,7 @@ _SIGNATURES = {
     "fa_selftest_division": (_I, [_I64, ctypes.c_uint64, _P, _P, _P]),
     "fa_set_kernel_timer": (_I, [_P, _P]),
     "fa_write_matrix_market": (_I, [ctypes.c_char_p, _I64, _I64, _P, _P, _P, _I]),
+    "fa_read_mesh_text": (_I, [ctypes.c_char_p, ctypes.POINTER(_I64), ctypes.POINTER(_I64), _P, _P, _I]),
 }
 
 _lib = None

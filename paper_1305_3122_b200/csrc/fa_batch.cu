@@ -127,9 +127,50 @@ __global__ void k_areas(const int32_t* __restrict__ me, int64_t nme, const doubl
     }
 }
 
+// Mesh ingestion (femasm Mesh.__init__, mesh.py:84-119, and compute_areas, mesh.py:51-69) in one
+// pass over the int64 connectivity: range check (first bad flattened position), repeated ids
+// (first triangle), int32 copy for the assembly plans, areas (bitwise compute_areas) and the first
+// degenerate triangle.  Triangles with a bad id get area 0 and are not reported as degenerate
+// (the reference raises the range / repeat errors first).
+__global__ void k_ingest(const int64_t* __restrict__ me64, int64_t nme, int64_t nq, const double2* __restrict__ q,
+                         int32_t* __restrict__ me32, double* __restrict__ areas, fa_result* res) {
+    for (int64_t k = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; k < nme; k += int64_t(gridDim.x) * blockDim.x) {
+        const int64_t c0 = me64[3 * k], c1 = me64[3 * k + 1], c2 = me64[3 * k + 2];
+        const bool r0 = c0 >= 0 && c0 < nq, r1 = c1 >= 0 && c1 < nq, r2 = c2 >= 0 && c2 < nq;
+        if (!r0) atomic_min_i64(&res->index_error_pos, 3 * k);
+        else if (!r1) atomic_min_i64(&res->index_error_pos, 3 * k + 1);
+        else if (!r2) atomic_min_i64(&res->index_error_pos, 3 * k + 2);
+        if (c0 == c1 || c1 == c2 || c0 == c2) atomic_min_i64(&res->repeat_error_pos, k);
+        me32[3 * k] = int32_t(c0);
+        me32[3 * k + 1] = int32_t(c1);
+        me32[3 * k + 2] = int32_t(c2);
+        double a = 0.0;
+        if (r0 && r1 && r2) {
+            a = tri_area(q[c0], q[c1], q[c2]);
+            if (a <= AREA_EPS) atomic_min_i64(&res->degenerate_index, k);
+        }
+        areas[k] = a;
+    }
+}
+
 }  // namespace fa
 
 using namespace fa;
+
+extern "C" int fa_mesh_ingest(const int64_t* d_me64, int64_t nme, int64_t nq, const double* d_q, int32_t* d_me32,
+                              double* d_areas, fa_result* d_res, void* stream) {
+    if (nme < 0 || nq < 1 || !d_me64 || !d_q || !d_me32 || !d_areas || !d_res) {
+        set_error("fa_mesh_ingest: bad argument"); return FA_ERR_ARGUMENT;
+    }
+    if (nq > INT32_MAX) { set_error("fa_mesh_ingest: nq=%lld beyond 32-bit vertex ids", (long long)nq); return FA_ERR_TOO_LARGE; }
+    cudaStream_t st = as_stream(stream);
+    k_result_reset<<<1, 32, 0, st>>>(d_res);
+    if (nme == 0) return FA_OK;
+    const int tb = 256;
+    k_ingest<<<grid_for(nme, tb), tb, 0, st>>>(d_me64, nme, nq, reinterpret_cast<const double2*>(d_q), d_me32, d_areas, d_res);
+    FA_LAUNCH_CHECK("k_ingest");
+    return FA_OK;
+}
 
 extern "C" int fa_element_kg(int kind, const int32_t* d_me, int64_t nme, const double* d_q, const double* d_areas,
                              const double* d_w, double lam, double mu, double* d_kg, fa_result* d_res, void* stream) {

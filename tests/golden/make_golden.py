@@ -6,6 +6,7 @@ the committed outputs.
     python tests/golden/make_golden.py digests C1 C2   -> tests/golden/reference_digests.json
     python tests/golden/make_golden.py digests C5ALL    -> every C5 row block + the whole C5 digest
     python tests/golden/make_golden.py loops           -> tests/golden/loop_cases.npz
+    python tests/golden/make_golden.py mesh_text       -> tests/golden/mesh_text_cases.json
 
 small_cases.npz: seeded BASELINE-family meshes (tiny N), the reference's own generators
 (square / disk) and the reference's OptV2 output for every kind, as full arrays.
@@ -159,6 +160,50 @@ def loops():
     print("loop cases:", list(meshes))
 
 
+MESH_TEXT_CASES = {
+    "plain": "3 1\n0 0\n1 0\n0 1\n1 2 3\n",
+    "crlf_tabs_blank_tail": "3 1\r\n0\t0\r\n1.5e0 -0\r\n.25   1.\r\n1 2 3\r\n\r\n   \r\n",
+    "python_tokens": "3 1\n+0 0\n1_0 0\ninf 1\n+1 0_2 3\n",
+    "empty": "",
+    "blank_header": "  \n3 1\n",
+    "header_fields": "3\n0 0\n",
+    "header_int": "3 x\n",
+    "counts": "0 1\n",
+    "short": "3 1\n0 0\n1 0\n",
+    "coords_count": "3 1\n0 0\n1 0 0\n0 1\n1 2 3\n",
+    "coord_value": "3 1\n0 0\n1 zz\n0 1\n1 2 3\n",
+    "tri_fields": "3 1\n0 0\n1 0\n0 1\n1 2\n",
+    "tri_int": "3 1\n0 0\n1 0\n0 1\n1 2 3.0\n",
+    "tri_range": "3 1\n0 0\n1 0\n0 1\n1 2 4\n",
+    "trailing": "3 1\n0 0\n1 0\n0 1\n1 2 3\n\nextra\n",
+    "invalid_mesh": "3 1\n0 0\n1 0\n0 1\n1 1 3\n",
+    "degenerate": "3 1\n0 0\n1 0\n2 0\n1 2 3\n",
+    "hex_float": "3 1\n0x1p0 0\n1 0\n0 1\n1 2 3\n",
+    "form_feed": "3 1\n0 0\n1 0\f\n0 1\n1 2 3\n",
+}
+
+
+def mesh_text():
+    """femasm.read_mesh on small text files -> tests/golden/mesh_text_cases.json: the arrays it
+    returns or the MeshFormatError (line number and message, path replaced by '<path>')."""
+    import tempfile
+
+    out = {}
+    d = Path(tempfile.mkdtemp())
+    for name, text in MESH_TEXT_CASES.items():
+        p = d / f"{name}.txt"
+        p.write_bytes(text.encode("ascii"))
+        try:
+            m = femasm.read_mesh(p)
+            out[name] = {"text": text, "ok": True, "vertices": m.vertices.tolist(),
+                         "connectivity": m.connectivity.tolist()}
+        except femasm.MeshFormatError as exc:
+            out[name] = {"text": text, "ok": False, "line_no": exc.line_no,
+                         "message": str(exc).replace(str(p), "<path>")}
+    (HERE / "mesh_text_cases.json").write_text(json.dumps(out, indent=1, sort_keys=True))
+    print("mesh text cases:", {k: v["ok"] for k, v in out.items()})
+
+
 def digests(names):
     path = HERE / "reference_digests.json"
     data = json.loads(path.read_text()) if path.exists() else {}
@@ -306,5 +351,7 @@ if __name__ == "__main__":
         small()
     elif sys.argv[1] == "loops":
         loops()
+    elif sys.argv[1] == "mesh_text":
+        mesh_text()
     elif sys.argv[1] == "digests":
         digests(sys.argv[2:])

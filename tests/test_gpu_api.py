@@ -306,3 +306,48 @@ def test_paper_entry_point_rejects_out_of_range_ids(golden, kind):
     m = call(C)  # the device is still healthy
     ref = tuple(golden[f"{name}/{kind}/{f}"] for f in ("col_ptr", "row_idx", "values"))
     assert_same_csc((m.col_ptr, m.row_idx, m.values), ref, kind)
+
+
+def test_read_mesh_matches_reference_end_to_end(tmp_path):
+    """read_mesh (native parser or reference rules, then the device Mesh ingestion) gives
+    femasm.read_mesh's arrays or its exact MeshFormatError for every golden text case."""
+    import json
+
+    from conftest import GOLDEN
+
+    cases = json.loads((GOLDEN / "mesh_text_cases.json").read_text())
+    for name, case in cases.items():
+        p = tmp_path / f"{name}.txt"
+        p.write_bytes(case["text"].encode("ascii"))
+        if case["ok"]:
+            m = fa.read_mesh(p)
+            assert np.array_equal(m.vertices, np.array(case["vertices"])), name
+            assert np.array_equal(m.connectivity, np.array(case["connectivity"])), name
+        else:
+            with pytest.raises(fa.MeshFormatError) as ei:
+                fa.read_mesh(p)
+            assert ei.value.line_no == case["line_no"], name
+            assert str(ei.value).replace(str(p), "<path>") == case["message"], name
+
+
+def test_mesh_ingestion_errors_in_reference_order():
+    """Mesh(V, C) validates on the device (fa_mesh_ingest) with mesh.py:87-113's messages and
+    order: range before repeated ids before degenerate areas; areas bitwise compute_areas."""
+    V = np.array([[0.0, 0.0], [1.0, 0.0], [0.0, 1.0], [2.0, 0.0]])
+    with pytest.raises(ValueError, match=r"connectivity index out of range \[0, nq\)"):
+        fa.Mesh(V, np.array([[0, 1, 1], [0, 1, 4]]))  # repeated AND out of range: range wins
+    with pytest.raises(ValueError, match="triangle with repeated vertex indices"):
+        fa.Mesh(V, np.array([[0, 1, 2], [0, 3, 3]]))
+    with pytest.raises(fa.DegenerateTriangleError) as ei:
+        fa.Mesh(V, np.array([[0, 1, 2], [0, 1, 3], [0, 3, 1]]))
+    assert ei.value.index == 1 and ei.value.area == 0.0
+    with pytest.raises(ValueError, match=r"connectivity index out of range \[0, nq\)"):
+        fa.Mesh(V, np.array([[0, 1, -1]]))
+    from oracle import femasm_oracle as fo
+    from paper_1305_3122_b200.meshgen import seeded_square_mesh
+
+    sm = seeded_square_mesh(64, 2)
+    m = fa.Mesh(sm.vertices, sm.connectivity)
+    assert np.array_equal(m.areas.view(np.int64), fo.triangle_areas(sm.vertices, sm.connectivity).view(np.int64))
+    me, q, a = m.device_arrays()
+    assert np.array_equal(me.cpu().numpy(), sm.connectivity.astype(np.int32))

@@ -138,3 +138,57 @@ def test_product_package_never_imports_the_oracle():
     for f in pkg.rglob("*.py"):
         text = f.read_text()
         assert "import oracle" not in text and "from oracle" not in text, f
+
+
+def _mesh_text_cases():
+    import json
+
+    from conftest import GOLDEN
+
+    return json.loads((GOLDEN / "mesh_text_cases.json").read_text())
+
+
+def test_mesh_text_parsers_match_reference(tmp_path):
+    """read_mesh's two parsers against femasm.read_mesh's own results (tests/golden/
+    mesh_text_cases.json, make_golden.py mesh_text): the native multithreaded one accepts the
+    well-formed layout and defers everything else; the reference-equivalent one returns the
+    same arrays or raises the same MeshFormatError (line number and text)."""
+    from paper_1305_3122_b200 import mesh as M
+
+    for name, case in _mesh_text_cases().items():
+        p = tmp_path / f"{name}.txt"
+        p.write_bytes(case["text"].encode("ascii"))
+        native = M._read_mesh_native(p)
+        mesh_error = not case["ok"] and "invalid mesh:" in case["message"]
+        if case["ok"] or mesh_error:
+            V, C = M._parse_mesh_text(p)
+            if case["ok"]:
+                assert np.array_equal(V, np.array(case["vertices"])), name
+                assert np.array_equal(C, np.array(case["connectivity"])), name
+            if native is not None:
+                assert np.array_equal(native[0], V) and np.array_equal(native[1], C), name
+            else:
+                assert name == "python_tokens", f"{name}: well-formed file rejected by the native parser"
+        else:
+            assert native is None, name
+            with pytest.raises(M.MeshFormatError) as ei:
+                M._parse_mesh_text(p)
+            assert ei.value.line_no == case["line_no"], name
+            assert str(ei.value).replace(str(p), "<path>") == case["message"], name
+
+
+def test_native_mesh_reader_large_file(tmp_path):
+    """A seeded mesh written with write_mesh's format parses natively to the same arrays."""
+    from paper_1305_3122_b200 import mesh as M
+    from paper_1305_3122_b200.meshgen import seeded_square_mesh
+
+    sm = seeded_square_mesh(120, 3)
+    p = tmp_path / "m.txt"
+    with open(p, "w") as f:
+        f.write(f"{sm.nq} {sm.nme}\n")
+        for x, y in sm.vertices:
+            f.write("%.17g %.17g\n" % (x, y))
+        for a, b, c in sm.connectivity:
+            f.write(f"{a + 1} {b + 1} {c + 1}\n")
+    V, C = M._read_mesh_native(p)
+    assert np.array_equal(V, sm.vertices) and np.array_equal(C, sm.connectivity)

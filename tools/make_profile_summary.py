@@ -34,19 +34,29 @@ stalls = {}
 for rep in reps:
     out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rr = list(csv.reader(out.splitlines()))
-    hh = rr[0]
+    hh, units = rr[0], rr[1]
+    SCALE = {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3, "Tbyte": 1e6,   # -> MB
+             "nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3, "second": 1e6,         # -> us
+             "ns": 1e-3, "us": 1.0, "ms": 1e3, "s": 1e6}
+    def conv(m, raw):
+        u = units[hh.index(m)]
+        try:
+            x = float(raw.replace(",", ""))
+        except ValueError:
+            return raw
+        return f"{x * SCALE.get(u, 1.0):.6g}" if u in SCALE else f"{x:.6g}"
     for v in rr[2:]:
         name = v[hh.index("Kernel Name")].split("(")[0].replace("void ", "")
-        full[name] = {lab: v[hh.index(m)] for m, lab in M.items() if m in hh}
+        full[name] = {lab: conv(m, v[hh.index(m)]) for m, lab in M.items() if m in hh}
         st = [(c.replace("smsp__average_warps_issue_stalled_", "").replace("_per_issue_active.ratio", ""), float(v[i] or 0))
               for i, c in enumerate(hh) if c.startswith("smsp__average_warps_issue_stalled_") and c.endswith("_per_issue_active.ratio")]
         stalls[name] = sorted(st, key=lambda x: -x[1])[:6]
 
 tot = sum(sum(v) / len(v) for v in ours.values())
 md = [f"# ncu summary, {tag}, config {cfg}", "",
-      f"Command: `python bench.py --steps 3 --warmup 3 --cpu-baseline-runs 0 --e2e-steps 1` (config {cfg}).",
-      "Launch list: `ncu --metrics gpu__time_duration.sum --clock-control none` (cold-cache, serialised);",
-      "per-kernel metrics: `ncu --set full --import-source on --clock-control none` (one launch each).", "",
+      f"Commands (config {cfg}): launch list `ncu --metrics gpu__time_duration.sum --clock-control none -c 400 python bench.py --config {cfg} --steps 2 --warmup 1 --e2e-steps 0 --cpu-baseline-runs 0 --verify 0` (graph replay: the warm steps are in the list too);",
+      f"full: `ncu --set full --import-source on --clock-control none -k regex:k_rows -c 1 python bench.py --config {cfg} --steps 1 --warmup 1 --e2e-steps 0 --cpu-baseline-runs 0 --verify 0 --graph 0` (bench mode: recomputed areas for stiffness/elasticity).",
+      "Launch-list times are cold-cache and serialised: compare shares, not absolutes.", "",
       "## Per-step launch list (average over launches)", "", "| kernel | launches | avg us | share of step |", "|---|---|---|---|"]
 for k, v in ours.items():
     a = sum(v) / len(v)
