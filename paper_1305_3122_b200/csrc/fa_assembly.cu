@@ -62,6 +62,21 @@ constexpr int CAPB_E = 7 * BV;     // elasticity: 12 values per incidence, two b
 constexpr int CAPB_W = 7 * BV;
 constexpr int ROWS_MINB = 4, ROWS_MINB_W = 5, ROWS_MINB_E = 2;
 constexpr int ROWS_AU = 3, ROWS_AU_W = 3, ROWS_AU_E = 1;
+// stiffness: five blocks per SM (<= 102 registers, two incidences in flight per thread in phase
+// a) and 832 incidences per bucket (6.5 per vertex: the mean degree is below 6, so overflowing
+// buckets stay rare) - the smaller shared-memory carve-out leaves L1 the room that keeps a row's
+// second gather of each neighbour (n1 of one incidence, n2 of the next) out of DRAM at C5
+// (C3 numeric 853 -> 753 us, C5 15.2 -> 13.8 ms against four blocks of 1024 incidences)
+#ifndef FA_STIFF_MINB
+#define FA_STIFF_MINB 5
+#endif
+#ifndef FA_STIFF_CAP
+#define FA_STIFF_CAP 832
+#endif
+#ifndef FA_STIFF_AU
+#define FA_STIFF_AU 2
+#endif
+constexpr int ROWS_MINB_S = FA_STIFF_MINB, CAPB_S = FA_STIFF_CAP, ROWS_AU_S = FA_STIFF_AU;
 constexpr int MAXD = 8;            // incidences per row on the register fast path
 constexpr int PLOG0 = 10;          // log2 of the minimum part size (vertices)
 constexpr int MAX_PARTS = 8192;
@@ -752,9 +767,10 @@ struct KindTraits {
     // entries of its two dof rows (own, n1, n2 vertex columns, x and y)
     static constexpr int RVALS = KIND == FA_KIND_ELASTIC ? 12 : 3;
     static constexpr int MIN_BLOCKS =
-        KIND == FA_KIND_ELASTIC ? ROWS_MINB_E : (KIND == FA_KIND_MASSW ? ROWS_MINB_W : ROWS_MINB);
+        KIND == FA_KIND_ELASTIC ? ROWS_MINB_E
+                                : (KIND == FA_KIND_MASSW ? ROWS_MINB_W : (KIND == FA_KIND_STIFF ? ROWS_MINB_S : ROWS_MINB));
     static constexpr int CAP =  // incidences in shared memory
-        KIND == FA_KIND_ELASTIC ? CAPB_E : (KIND == FA_KIND_MASSW ? CAPB_W : CAPB);
+        KIND == FA_KIND_ELASTIC ? CAPB_E : (KIND == FA_KIND_MASSW ? CAPB_W : (KIND == FA_KIND_STIFF ? CAPB_S : CAPB));
     static constexpr size_t REC_BYTES = size_t(CAP) * (RVALS * 8 + 12);
     static constexpr int STAGE = int(REC_BYTES / 12);  // staged entries fitting the records area
 };
@@ -794,7 +810,7 @@ __device__ __forceinline__ Gathered gather_incidence(const RowsArgs& A, unsigned
 // reported (assembly.py:152-155) for every kind that divides by the area.
 template <int KIND>
 __device__ __forceinline__ void incidence_values(const RowsArgs& A, unsigned k, int a, const Gathered& g,
-                                                 double2 own_p, double own_w, double* out) {
+                                                 double2 own_p, double* out) {
     double ar = g.ar;
     double2 c0, c1, c2;  // corners in triangle order (area recomputation, elasticity)
     if (KIND == FA_KIND_ELASTIC || !A.areas) {
@@ -928,7 +944,7 @@ struct RowCount {
 // zeros kept (removed later by k_compact) or dropped per `keep_zeros`; zero sums counted.
 template <int KIND>
 __device__ __noinline__ RowCount general_row(const RowsArgs& A, BucketRecs R, bool overflow, int64_t gfirst, int start,
-                                             int deg, int64_t v, double2 own_p, double own_w, int s, int64_t out_pos,
+                                             int deg, int64_t v, double2 own_p, int s, int64_t out_pos,
                                              bool values, bool write = true, bool keep_zeros = true) {
     constexpr int NV = KindTraits<KIND>::NV;
     constexpr int RVALS = KindTraits<KIND>::RVALS;
@@ -950,7 +966,7 @@ __device__ __noinline__ RowCount general_row(const RowsArgs& A, BucketRecs R, bo
         n2 = int(A.sn2[gfirst + i]);
         if (need_vals) {
             const Gathered g = gather_incidence<KIND>(A, ka >> 2, unsigned(n1), unsigned(n2), l2_evict_last_policy());
-            incidence_values<KIND>(A, ka >> 2, a, g, own_p, own_w, rv);
+            incidence_values<KIND>(A, ka >> 2, a, g, own_p, rv);
         }
     };
     int64_t last = -1, count = 0, zeros = 0;
@@ -1100,7 +1116,6 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     __shared__ unsigned char s_own[TR::CAP];
     __shared__ int s_vst[BV + 1];
     __shared__ double2 s_oq[BV];
-    __shared__ double s_ow[BV];
     __shared__ int64_t s_tile;
     __shared__ uint64_t s_prefix;
     __shared__ int64_t s_warp[NT / 32];
@@ -1145,7 +1160,6 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     for (int i = tid; i < BV; i += NT) {
         const int64_t vv = vbase + i;
         s_oq[i] = (need_q && A.q && vv < A.v1) ? A.q[vv] : make_double2(0.0, 0.0);
-        s_ow[i] = 0.0;  // (the weighted mass reads its W per triangle, k_tri_wt)
     }
     __syncthreads();
     for (int vl = tid; vl < nvb && !overflow; vl += NT)
@@ -1196,7 +1210,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         count = deg == 0 ? 0 : int64_t(NV) * (distinct + 1);  // no triplet, no entry (isolated vertex)
     }
     if (EARLY && slow)
-        count = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc], s_ow[vloc], s, 0,
+        count = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc], s, 0,
                                   false).count;
     if (EARLY) {
         excl = block_exclusive_scan_1b<NT>(count, s_warp, total);
@@ -1206,7 +1220,8 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     // ---- a) per incidence (balanced over threads): gathers from the L2-resident arrays, the
     //         row of the element matrix -> shared memory
     {
-        constexpr int AU = KIND == FA_KIND_ELASTIC ? ROWS_AU_E : (KIND == FA_KIND_MASSW ? ROWS_AU_W : ROWS_AU);
+        constexpr int AU = KIND == FA_KIND_ELASTIC ? ROWS_AU_E
+                                                   : (KIND == FA_KIND_MASSW ? ROWS_AU_W : (KIND == FA_KIND_STIFF ? ROWS_AU_S : ROWS_AU));
         for (int i0 = tid; i0 < n; i0 += NT * AU) {
             unsigned ka[AU];
             Gathered g[AU];
@@ -1222,7 +1237,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
                 if (i >= n) break;
                 const int vl = s_own[i];
                 double rv[RVALS];
-                incidence_values<KIND>(A, ka[u] >> 2, int(ka[u] & 3u), g[u], s_oq[vl], s_ow[vl], rv);
+                incidence_values<KIND>(A, ka[u] >> 2, int(ka[u] & 3u), g[u], s_oq[vl], rv);
                 if constexpr (KIND == FA_KIND_ELASTIC) {
 #pragma unroll
                     for (int j = 0; j < RVALS; ++j) R.vals[j * CAP + i] = rv[j];
@@ -1268,8 +1283,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
             const int64_t o = int64_t(base) + excl;
             if (fast) zeros = walk_row<KIND, true>(R, sk, start, deg, vv, dpos, A.col + o, A.val + o, A.capacity - o);
             if (slow)
-                zeros = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc],
-                                          s_ow[vloc], s, o, true, true, true)
+                zeros = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc], s, o, true, true, true)
                             .zeros;
         }
     } else {
@@ -1336,8 +1350,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     }
     if (!EARLY) {
         if (slow) {
-            const RowCount rc = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc],
-                                                  s_ow[vloc], s, 0, true, false, false);
+            const RowCount rc = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc], s, 0, true, false, false);
             count = rc.count;
             zeros = rc.zeros;
         }
@@ -1430,8 +1443,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
             }
         }
         if (slow) {
-            const RowCount rc = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc],
-                                                  s_ow[vloc], s, int64_t(base) + excl, true, true, EARLY);
+            const RowCount rc = general_row<KIND>(A, R, overflow, int64_t(gbase) + start, start, deg, v, s_oq[vloc], s, int64_t(base) + excl, true, true, EARLY);
             if (EARLY) zeros = rc.zeros;
         }
     }

@@ -17,6 +17,9 @@ dev = torch.device("cuda")
 me = torch.from_numpy(sm.connectivity.astype(np.int32)).to(dev)
 q = torch.from_numpy(sm.vertices).to(dev)
 a = torch.from_numpy(fa.compute_areas(sm.vertices, sm.connectivity)).to(dev)
+import os
+if os.environ.get("RECOMPUTE", "1") == "1" and kind in ("stiff", "elastic"):
+    a = None  # bench mode: areas recomputed in the row kernel
 w = torch.from_numpy(sm.weights).to(dev) if kind == "massw" else None
 from paper_1305_3122_b200.dist import row_blocks
 v0, v1 = row_blocks(sm.nq, G)[0]
