@@ -82,16 +82,37 @@ constexpr int PLOG0 = 10;          // log2 of the minimum part size (vertices)
 constexpr int MAX_PARTS = 8192;
 constexpr int PLAN_THREADS = 1024;
 constexpr int SORT_THREADS = 512;   // k_part_sort (2 blocks / SM, 64 registers)
-constexpr int PLACE_THREADS = 1024;  // k_part_hist / k_part_place block size
-constexpr int PLACE_BLOCKS_PER_SM = 1;
-constexpr int PLACE_TRI = 2048;    // triangles per placement round
+#ifndef FA_PLACE_THREADS
+#define FA_PLACE_THREADS 1024
+#endif
+#ifndef FA_PLACE_MINB
+#define FA_PLACE_MINB 1
+#endif
+#ifndef FA_PLACE_TRI
+#define FA_PLACE_TRI 2048
+#endif
+constexpr int PLACE_THREADS = FA_PLACE_THREADS;  // k_part_hist / k_part_place block size
+constexpr int PLACE_BLOCKS_PER_SM = FA_PLACE_MINB;
+constexpr int PLACE_TRI = FA_PLACE_TRI;    // triangles per placement round
 constexpr int SPLIT_MIN = 8192;    // fine parts above which placement goes through coarse parts
 // records above this size do not stay in L2 between placement and sort, so the placement's
 // runs must be long (coarse parts) and a parallel split regroups them by fine part
 constexpr int64_t SPLIT_BYTES = int64_t(160) << 20;
 constexpr int SPLIT_COARSE = 256;  // coarse parts of a two-level plan (at most)
 constexpr int FINE_HIST_MAX = 98304;  // fine parts counted in k_part_hist's shared memory (16 bit)
-constexpr int SPLIT2_LOCAL = 1024;    // fine parts a k_part_split round ranks in shared memory
+#ifndef FA_SPLIT_THREADS
+#define FA_SPLIT_THREADS 512
+#endif
+#ifndef FA_SPLIT_RI
+#define FA_SPLIT_RI 4096
+#endif
+#ifndef FA_SPLIT_MINB
+#define FA_SPLIT_MINB 2
+#endif
+constexpr int SPLIT_THREADS = FA_SPLIT_THREADS;
+constexpr int SPLIT_RI = FA_SPLIT_RI;       // records per k_part_split round
+constexpr int SPLIT_MINB = FA_SPLIT_MINB;   // k_part_split blocks per SM
+constexpr int SPLIT2_LOCAL = SPLIT_THREADS;  // fine parts a k_part_split round ranks in shared memory
 constexpr int SORT_CAP = 7680;     // part incidences sorted in shared memory (2 blocks / SM)
 
 // Resets the result block and zeroes the counters the following kernels accumulate into
@@ -438,20 +459,18 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
     }
 }
 
-constexpr int SPLIT_THREADS = 1024;
-
 // K3b (two-level plans): the placement's records regrouped by fine part,
 // in parallel over rounds of 3 * PLACE_TRI consecutive records (any block, any coarse part):
 // ranked by fine part in shared memory (relative to the round's smallest fine part), one range
 // per fine part reserved from the global cursors (K2), staged and written as coalesced runs.
 // Records whose fine part lies beyond the local window (only when coarse parts are smaller
 // than a round) take a cursor each.
-__global__ void __launch_bounds__(SPLIT_THREADS, 1)
+__global__ void __launch_bounds__(SPLIT_THREADS, SPLIT_MINB)
     k_part_split(const uint4* __restrict__ rec, const unsigned* __restrict__ total_ptr, int plog,
                   unsigned* __restrict__ fine_fill, uint4* __restrict__ rec2) {
     pdl_enter();
     extern __shared__ __align__(16) unsigned char smem_raw[];
-    constexpr int RI = 3 * PLACE_TRI;
+    constexpr int RI = SPLIT_RI;
     constexpr int PER = RI / SPLIT_THREADS;
     uint4* s_stage = reinterpret_cast<uint4*>(smem_raw);                       // [RI]
     unsigned* s_cnt = reinterpret_cast<unsigned*>(s_stage + RI);             // [SPLIT2_LOCAL]
@@ -1902,14 +1921,14 @@ static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* s
     FA_CUDA(cudaFuncSetAttribute(k_part_place, cudaFuncAttributeMaxDynamicSharedMemorySize, int(place_smem)));
     FA_CUDA(launch_pdl(pdl ? 3 : -1, k_part_place, dim3(p->nblk_place), dim3(PLACE_THREADS), place_smem, st, P));
     if (p->fine_hist) {
-        constexpr int RI = 3 * PLACE_TRI;
+        constexpr int RI = SPLIT_RI;
         const size_t split_smem = size_t(RI) * (sizeof(uint4) + sizeof(unsigned short)) + sizeof(unsigned) * 3 * SPLIT2_LOCAL;
         FA_CUDA(cudaFuncSetAttribute(k_part_split, cudaFuncAttributeMaxDynamicSharedMemorySize, int(split_smem)));
         int nsm = 0, dev = 0;
         FA_CUDA(cudaGetDevice(&dev));
         FA_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev));
         const int64_t rounds = (3 * p->nme + RI - 1) / RI;  // upper bound on the owned incidences
-        const unsigned grid = unsigned(rounds < nsm ? rounds : nsm);
+        const unsigned grid = unsigned(rounds < int64_t(nsm) * SPLIT_MINB ? rounds : int64_t(nsm) * SPLIT_MINB);
         FA_CUDA(launch_pdl(pdl ? 4 : -1, k_part_split, dim3(grid), dim3(SPLIT_THREADS), split_smem, st, p->rec,
                            p->part_off + p->nparts, p->plog, p->fine_fill, p->rec2));
     }
