@@ -55,7 +55,7 @@ namespace fa {
 constexpr int BV = 128;            // vertices per row bucket
 // row kernel shape per kind: incidences held in shared memory per bucket (CAP), blocks per SM
 // (register budget), incidences / W records in flight per thread in phase a (AU)
-constexpr int CAPB = 8 * BV;       // mass, stiffness: <= 128 registers, four blocks per SM
+constexpr int CAPB = 8 * BV;       // mass: <= 128 registers, four blocks per SM
 constexpr int CAPB_E = 7 * BV;     // elasticity: 12 values per incidence, two blocks per SM
 // weighted mass (five blocks per SM, <= 102 registers): a smaller bucket leaves L1 more room; the
 // mean degree of a planar triangulation is below 6, so overflowing buckets (general path) stay rare
@@ -67,51 +67,27 @@ constexpr int ROWS_AU = 3, ROWS_AU_W = 3, ROWS_AU_E = 1;
 // buckets stay rare) - the smaller shared-memory carve-out leaves L1 the room that keeps a row's
 // second gather of each neighbour (n1 of one incidence, n2 of the next) out of DRAM at C5
 // (C3 numeric 853 -> 753 us, C5 15.2 -> 13.8 ms against four blocks of 1024 incidences)
-#ifndef FA_STIFF_MINB
-#define FA_STIFF_MINB 5
-#endif
-#ifndef FA_STIFF_CAP
-#define FA_STIFF_CAP 832
-#endif
-#ifndef FA_STIFF_AU
-#define FA_STIFF_AU 2
-#endif
-constexpr int ROWS_MINB_S = FA_STIFF_MINB, CAPB_S = FA_STIFF_CAP, ROWS_AU_S = FA_STIFF_AU;
+constexpr int ROWS_MINB_S = 5, CAPB_S = 832, ROWS_AU_S = 2;
 constexpr int MAXD = 8;            // incidences per row on the register fast path
 constexpr int PLOG0 = 10;          // log2 of the minimum part size (vertices)
 constexpr int MAX_PARTS = 8192;
 constexpr int PLAN_THREADS = 1024;
 constexpr int SORT_THREADS = 512;   // k_part_sort (2 blocks / SM, 64 registers)
-#ifndef FA_PLACE_THREADS
-#define FA_PLACE_THREADS 1024
-#endif
-#ifndef FA_PLACE_MINB
-#define FA_PLACE_MINB 1
-#endif
-#ifndef FA_PLACE_TRI
-#define FA_PLACE_TRI 2048
-#endif
-constexpr int PLACE_THREADS = FA_PLACE_THREADS;  // k_part_hist / k_part_place block size
-constexpr int PLACE_BLOCKS_PER_SM = FA_PLACE_MINB;
-constexpr int PLACE_TRI = FA_PLACE_TRI;    // triangles per placement round
+constexpr int PLACE_THREADS = 1024;  // k_part_hist / k_part_place block size
+constexpr int PLACE_BLOCKS_PER_SM = 1;
+constexpr int PLACE_TRI = 2048;    // triangles per placement round
 constexpr int SPLIT_MIN = 8192;    // fine parts above which placement goes through coarse parts
 // records above this size do not stay in L2 between placement and sort, so the placement's
 // runs must be long (coarse parts) and a parallel split regroups them by fine part
 constexpr int64_t SPLIT_BYTES = int64_t(160) << 20;
 constexpr int SPLIT_COARSE = 256;  // coarse parts of a two-level plan (at most)
 constexpr int FINE_HIST_MAX = 98304;  // fine parts counted in k_part_hist's shared memory (16 bit)
-#ifndef FA_SPLIT_THREADS
-#define FA_SPLIT_THREADS 512
-#endif
-#ifndef FA_SPLIT_RI
-#define FA_SPLIT_RI 4096
-#endif
-#ifndef FA_SPLIT_MINB
-#define FA_SPLIT_MINB 2
-#endif
-constexpr int SPLIT_THREADS = FA_SPLIT_THREADS;
-constexpr int SPLIT_RI = FA_SPLIT_RI;       // records per k_part_split round
-constexpr int SPLIT_MINB = FA_SPLIT_MINB;   // k_part_split blocks per SM
+// k_part_split: two blocks of 512 threads per SM, rounds of 4096 records (C5 split 3.37 ->
+// 2.5 ms against one block of 1024 threads with 6144-record rounds: a block's load, rank and
+// write phases overlap the other block's)
+constexpr int SPLIT_THREADS = 512;
+constexpr int SPLIT_RI = 4096;      // records per k_part_split round
+constexpr int SPLIT_MINB = 2;       // k_part_split blocks per SM
 constexpr int SPLIT2_LOCAL = SPLIT_THREADS;  // fine parts a k_part_split round ranks in shared memory
 constexpr int SORT_CAP = 7680;     // part incidences sorted in shared memory (2 blocks / SM)
 
@@ -653,10 +629,11 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_cons
     unsigned* n1 = fast ? s_dyn + PV + SORT_CAP : P.sn1 + off;
     unsigned* n2 = fast ? s_dyn + PV + 2 * SORT_CAP : P.sn2 + off;
     unsigned short* s_src = reinterpret_cast<unsigned short*>(s_dyn + PV + 3 * SORT_CAP);  // fast: [SORT_CAP]
-    for (unsigned i0 = tid; i0 < n; i0 += 4 * SORT_THREADS) {  // four records in flight per thread
-        uint4 r[4];
+    constexpr int RU = 6;  // records in flight per thread (C5 sort 3.50 -> 3.37 ms against four)
+    for (unsigned i0 = tid; i0 < n; i0 += RU * SORT_THREADS) {
+        uint4 r[RU];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < RU; ++u) {
             const unsigned i = i0 + u * SORT_THREADS;
             if (i < n)
                 asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
@@ -664,7 +641,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_cons
                              : "l"(P.rec + off + i), "l"(pol));
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) {
+        for (int u = 0; u < RU; ++u) {
             if (i0 + u * SORT_THREADS < n) {
                 const unsigned pos = atomicAdd(&s_cur[(r[u].y >> 2) & unsigned(PV - 1)], 1u);
                 key[pos] = (r[u].x << 2) | (r[u].y & 3u);

@@ -19,6 +19,7 @@ from paper_1305_3122_b200.meshgen import BASELINE_CONFIGS, seeded_square_mesh
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C5"
 reps = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+GS = [int(x) for x in sys.argv[3].split(",")] if len(sys.argv) > 3 else [1, 2, 4, 8]
 kind, n, lam, mu = BASELINE_CONFIGS[cfg]
 sm = seeded_square_mesh(n, 0)
 dev = torch.device("cuda")
@@ -31,7 +32,7 @@ w = torch.from_numpy(sm.weights).to(dev) if kind == "massw" else None
 flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
 s = torch.cuda.Stream()
 rows = []
-for G in (1, 2, 4, 8):
+for G in GS:
     times = []
     for rank, (v0, v1) in enumerate(row_blocks(sm.nq, G)):
         plan = fa.AssemblyPlan(sm.nme, sm.nq, v0, v1)
