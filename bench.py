@@ -425,6 +425,22 @@ def _allreduce(dist, t, op, gloo):
     return t
 
 
+def dist_info(world):
+    """Communicator facts for the JSON line (N > 1): backend, world size, NCCL version."""
+    if world == 1:
+        return None
+    import torch
+    import torch.distributed as dist
+
+    info = {"backend": dist.get_backend(), "world_size": dist.get_world_size(), "rank_of_printer": dist.get_rank()}
+    try:
+        v = torch.cuda.nccl.version()
+        info["nccl_version"] = ".".join(str(x) for x in v) if isinstance(v, tuple) else str(v)
+    except Exception:  # noqa: BLE001 - informational only
+        pass
+    return info
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
@@ -451,6 +467,9 @@ def run_ours(args):
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
+        # the communicator every rank sees (stderr; the JSON line repeats it under "dist")
+        print(f"[bench] rank {rank}/{world} backend={dist.get_backend()} world_size={dist.get_world_size()} "
+              f"device=cuda:{gpu}", file=sys.stderr, flush=True)
 
     kind, n, lam, mu, sm = mesh_for(args.config, args.seed)
     me32 = np.ascontiguousarray(sm.connectivity, dtype=np.int32)
@@ -485,18 +504,24 @@ def run_ours(args):
     torch.cuda.synchronize()
     lib = _lib.lib()
 
-    def step(cold=True):
+    def compute(cold=True):
         # current stream (the capture stream inside a graph capture)
         if cold:  # fa_assemble_cold: plan build + numeric pass (weighted mass: W records in the build)
             plan.assemble_cold_into(me_d, kind, q_use, a_d, w_d, lam, mu, rowptr, col, val, res)
         else:
             plan.assemble_into(kind, q_use, a_d, w_d, lam, mu, rowptr, col, val, res)
+
+    def exchange():
         if world > 1:
             if gloo:  # functional-check backend (CPU tensors)
                 parts = [torch.empty(1, dtype=torch.int64) for _ in range(world)]
                 dist.all_gather(parts, rowptr[-1:].cpu())
             else:
                 dist.all_gather_into_tensor(nnz_t, rowptr[-1:])  # row-offset allgather (NCCL)
+
+    def step(cold=True):
+        compute(cold)
+        exchange()
 
     # one cold (or warm) step captured as a CUDA graph: the launches of the ~9 kernels of a
     # step are replayed without host round trips (the kernel timer events are graph nodes)
@@ -508,18 +533,21 @@ def run_ours(args):
             side = torch.cuda.Stream()
             side.wait_stream(torch.cuda.current_stream())
             with torch.cuda.stream(side):
-                step(cold)  # warm the capture stream
+                compute(cold)  # warm the capture stream
             torch.cuda.current_stream().wait_stream(side)
             torch.cuda.synchronize()
             lib.fa_set_kernel_timer(ev_rows0.cuda_event, ev_rows1.cuda_event)
-            with torch.cuda.graph(g):
-                step(cold)
+            # thread-local capture: the NCCL watchdog thread's event queries stay legal
+            with torch.cuda.graph(g, capture_error_mode="thread_local" if world > 1 else "global"):
+                compute(cold)
             lib.fa_set_kernel_timer(None, None)
             torch.cuda.synchronize()
             graphs[cold] = g
         return graphs[cold]
 
-    use_graph = args.graph and world == 1  # (NCCL collectives stay eager for N > 1)
+    # the step's kernels replay as one CUDA graph at every N; for N > 1 the 8-byte NCCL nnz
+    # allgather follows the replay eagerly on the same stream (gloo: functional checks only)
+    use_graph = bool(args.graph) and not gloo
 
     def timed_loop(steps, cold):
         starts = [torch.cuda.Event(enable_timing=True) for _ in range(steps)]
@@ -531,6 +559,7 @@ def run_ours(args):
             starts[i].record()
             if g is not None:
                 g.replay()
+                exchange()
             else:
                 lib.fa_set_kernel_timer(ev_rows0.cuda_event, ev_rows1.cuda_event)
                 step(cold)
@@ -655,7 +684,9 @@ def run_ours(args):
             "parallelism": f"row-blocks x{world}" if world > 1 else "single GPU",
             "step": "cold: plan build (part histogram, placement, per-part vertex sort) + fused row kernel "
                     "(+ NCCL nnz allgather when N>1), from device-resident me/q",
-            "launch": "CUDA graph replay per step" if use_graph else "eager launches",
+            "launch": ("CUDA graph replay per step" + (" + eager NCCL nnz allgather" if world > 1 else ""))
+                      if use_graph else "eager launches",
+            "dist": dist_info(world),
             "parity": parity,
             "hbm_gbs_whole_step": ab_total / (total_ms / args.steps * 1e-3) / 1e9,
             "roofline": {"bound": "hbm", "kernel": "k_rows (fused element + sparse() row kernel)",
