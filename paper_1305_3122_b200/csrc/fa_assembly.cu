@@ -808,12 +808,17 @@ template <int KIND>
 __device__ __forceinline__ void incidence_values(const RowsArgs& A, unsigned k, int a, const Gathered& g,
                                                  double2 own_p, double* out) {
     double ar = g.ar;
-    double2 c0, c1, c2;  // corners in triangle order (area recomputation, elasticity)
-    if (KIND == FA_KIND_ELASTIC || !A.areas) {
-        c0 = sel3(a, own_p, g.p2, g.p1);
-        c1 = sel3(a, g.p1, own_p, g.p2);
-        c2 = sel3(a, g.p2, g.p1, own_p);
-        if (!A.areas) ar = tri_area(c0, c1, c2);
+    // elasticity: the edges opposite the own corner and the two neighbours (the reference's u,
+    // v, w in local order: same operands, same bits, assembly.py:195-211), and the area from
+    // them (bitwise compute_areas, tri_area_edges; C4 numeric -3 % against the corner selects)
+    double2 eo = make_double2(0.0, 0.0), e1 = eo, e2 = eo;
+    if (KIND == FA_KIND_ELASTIC) {
+        eo = dsub2(g.p1, g.p2);
+        e1 = dsub2(g.p2, own_p);
+        e2 = dsub2(own_p, g.p1);
+        if (!A.areas) ar = tri_area_edges(a, eo, e1, e2);
+    } else if (!A.areas) {  // corners in triangle order (compute_areas, mesh.py:62-65)
+        ar = tri_area(sel3(a, own_p, g.p2, g.p1), sel3(a, g.p1, own_p, g.p2), sel3(a, g.p2, g.p1, own_p));
     }
     if (KIND != FA_KIND_MASSW && ar <= AREA_EPS) atomic_min_i64(&A.res->degenerate_index, int64_t(k));
     if constexpr (KIND == FA_KIND_MASS) {
@@ -852,7 +857,6 @@ __device__ __forceinline__ void incidence_values(const RowsArgs& A, unsigned k, 
         // gradients of the own corner and the two neighbours from the edges opposite them (the
         // reference's u, v, w in local order: same operands, same bits, assembly.py:195-211)
         const double inv2a = FDIV(0.5, ar);
-        const double2 eo = dsub2(g.p1, g.p2), e1 = dsub2(g.p2, own_p), e2 = dsub2(own_p, g.p1);
         const double2 gO = make_double2(FMUL(eo.y, inv2a), FMUL(-eo.x, inv2a));
         const double L = A.lam, M = A.mu, P = FADD(A.lam, FMUL(2.0, A.mu));
         // own 2x2 block (elastic_lower with A == B; (x, y) is the copy of (y, x))

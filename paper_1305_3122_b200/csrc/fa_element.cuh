@@ -38,6 +38,17 @@ __device__ __forceinline__ double tri_area(double2 p1, double2 p2, double2 p3) {
     return FMUL(0.5, fabs(cross));
 }
 
+__device__ __forceinline__ double2 dsub2(double2 a, double2 b) { return make_double2(FSUB(a.x, b.x), FSUB(a.y, b.y)); }
+
+// compute_areas from the local edges of the corner at position a (eo = n1 - n2, e1 = n2 - own,
+// e2 = own - n1): the corner differences of the triangle-order formula are +-(e2, e1) (a = 0),
+// (e1, eo) (a = 1), (eo, e2) (a = 2); RN(-x) = -RN(x) makes the cross product the exact negation
+// of tri_area's and fabs removes the sign, so the result is bitwise tri_area(c0, c1, c2).
+__device__ __forceinline__ double tri_area_edges(int a, double2 eo, double2 e1, double2 e2) {
+    const double2 u = sel3(a, e2, e1, eo), v = sel3(a, e1, eo, e2);
+    return FMUL(0.5, fabs(FSUB(FMUL(u.x, v.y), FMUL(v.x, u.y))));
+}
+
 // ---- per-kind prepared triangle data ---------------------------------------------------
 
 struct MassTri {
@@ -91,7 +102,6 @@ struct StiffTri {
     double a4;           // 4.0 * area
     DivBy d4;            // division by a4 (reciprocal shared by the entries)
 };
-__device__ __forceinline__ double2 dsub2(double2 a, double2 b) { return make_double2(FSUB(a.x, b.x), FSUB(a.y, b.y)); }
 __device__ __forceinline__ StiffTri stiff_prepare(double2 p1, double2 p2, double2 p3, double area) {
     const double a4 = FMUL(4.0, area);
     return {dsub2(p2, p3), dsub2(p3, p1), dsub2(p1, p2), a4, div_prepare(a4)};
