@@ -213,13 +213,23 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
     if (threadIdx.x == 0) s_tn = 0;
     __syncthreads();
     const int64_t k0 = int64_t(blockIdx.x) * P.chunk, k1 = min(P.nme, k0 + P.chunk);
-    constexpr int U = 4;  // triangles in flight per thread
+    constexpr int U = 4;  // triangles per thread per iteration; the next iteration's are loaded
+                          // while these are counted
+    int nx[U][3];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+        const int64_t k = k0 + threadIdx.x + u * PLACE_THREADS;
+        if (k < k1) load_tri_ids(P.me, k, nx[u][0], nx[u][1], nx[u][2]);
+    }
     for (int64_t k0u = k0 + threadIdx.x; k0u < k1; k0u += U * PLACE_THREADS) {
         int c[U][3];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t k = k0u + u * PLACE_THREADS;
-            if (k < k1) load_tri_ids(P.me, k, c[u][0], c[u][1], c[u][2]);
+            c[u][0] = nx[u][0];
+            c[u][1] = nx[u][1];
+            c[u][2] = nx[u][2];
+            const int64_t k = k0u + (U + u) * PLACE_THREADS;
+            if (k < k1) load_tri_ids(P.me, k, nx[u][0], nx[u][1], nx[u][2]);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -228,7 +238,7 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
             // a triangle with an out-of-range corner is reported and left out entirely, so no
             // incidence ever names an invalid neighbour
             const bool ok = tri_ids_valid(c[u][0], c[u][1], c[u][2], P.nq);
-            if (P.tri && ok) {
+            if (P.tri && ok) {  // (same-address shared atomics of a warp are combined in hardware)
                 bool own = false;
 #pragma unroll
                 for (int a = 0; a < 3; ++a) own |= c[u][a] >= P.v0 && c[u][a] < P.v1;
