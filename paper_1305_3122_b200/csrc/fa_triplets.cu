@@ -6,9 +6,13 @@
 //   - range checks with the first offending position, rows before columns (:157-158)
 //   - input zeros ignored (:160-162): adding +-0.0 never changes a partial sum here and an
 //     all-zero position sums to 0.0 and is dropped, so zeros are carried, not filtered
-//   - code = col * n_rows + row (:164-165), STABLE sort (:166): LSD radix sort, each pass a
-//     stable counting sort (ranks by warp match + ordered per-warp counters)
-//   - per position, left-to-right sum in input order (:176): one thread per run, sequential
+//   - code = col * n_rows + row (:164-165), STABLE sort (:166): LSD radix sort of (code, value)
+//     pairs, 8-bit digits; each pass ranks a 4096-pair tile stably by digit in shared memory
+//     (warp match + ordered per-warp counters), stages it in digit order and writes every
+//     digit's run coalesced at its global offset (digit-major scan of the tile histograms)
+//   - per position, left-to-right sum in input order (:176): the sort is stable, so each run's
+//     values arrive in input order; one thread per run sums them sequentially (a tree or
+//     shuffle reduction would round differently)
 //   - exact-zero sums dropped (:177-179), row = code % n_rows, col = code / n_rows (:180-181)
 //   - col_ptr = cumulative column counts (:187-188)
 #include <climits>
@@ -21,10 +25,11 @@ constexpr int TS_BLOCK = 256;
 constexpr int TS_ROUNDS = 16;
 constexpr int TS_TILE = TS_BLOCK * TS_ROUNDS;
 constexpr int TS_RADIX = 256;
+constexpr size_t TS_STAGE_BYTES = size_t(TS_TILE) * (sizeof(uint64_t) + sizeof(double));  // k_trip_scatter staging
 
 struct TripletWs {
     uint64_t *key0, *key1;
-    int64_t *idx0, *idx1;
+    double *val0, *val1;
     int64_t* hist;      // TS_RADIX * ntiles (+1)
     int* flag;          // len
     int64_t* pos;       // len + 1
@@ -47,8 +52,8 @@ static size_t carve(TripletWs* w, void* base, int64_t len) {
     TripletWs t;
     t.key0 = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * n));
     t.key1 = reinterpret_cast<uint64_t*>(take(sizeof(uint64_t) * n));
-    t.idx0 = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * n));
-    t.idx1 = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * n));
+    t.val0 = reinterpret_cast<double*>(take(sizeof(double) * n));
+    t.val1 = reinterpret_cast<double*>(take(sizeof(double) * n));
     t.hist = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * (hist_n + 1)));
     t.flag = reinterpret_cast<int*>(take(sizeof(int) * (scan_n + 1)));
     t.pos = reinterpret_cast<int64_t*>(take(sizeof(int64_t) * (scan_n + 1)));
@@ -60,16 +65,16 @@ static size_t carve(TripletWs* w, void* base, int64_t len) {
     return off;
 }
 
-__global__ void k_trip_keys(const int64_t* __restrict__ rows, const int64_t* __restrict__ cols, int64_t len,
-                            int64_t n_rows, int64_t n_cols, uint64_t* __restrict__ key, int64_t* __restrict__ idx,
-                            fa_result* res) {
+__global__ void k_trip_keys(const int64_t* __restrict__ rows, const int64_t* __restrict__ cols,
+                            const double* __restrict__ vals, int64_t len, int64_t n_rows, int64_t n_cols,
+                            uint64_t* __restrict__ key, double* __restrict__ val, fa_result* res) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < len; i += int64_t(gridDim.x) * blockDim.x) {
         const int64_t r = rows[i], c = cols[i];
         const bool rbad = r < 0 || r >= n_rows, cbad = c < 0 || c >= n_cols;
         if (rbad) atomic_min_i64(&res->index_error_pos, i);
         if (cbad) atomic_min_i64(&res->col_error_pos, i);
         key[i] = (rbad || cbad) ? 0 : uint64_t(c) * uint64_t(n_rows) + uint64_t(r);
-        idx[i] = i;
+        val[i] = vals[i];
     }
 }
 
@@ -113,53 +118,82 @@ __global__ void __launch_bounds__(256) k_scan_i64_inplace(int64_t* __restrict__ 
     if (base <= n - 1 && n - 1 < base + 8) a[n] = run;
 }
 
-__global__ void __launch_bounds__(TS_BLOCK) k_trip_scatter(const uint64_t* __restrict__ kin, const int64_t* __restrict__ iin,
-                                                            uint64_t* __restrict__ kout, int64_t* __restrict__ iout,
+// One stable counting-sort pass over a tile of TS_TILE (code, value) pairs: the tile's digit
+// histogram and its exclusive scan, then rounds of TS_BLOCK pairs in input order ranked by
+// digit (warp match for the rank among equal digits of a warp, per-warp counters ordered
+// across warps), each pair staged at its tile-local sorted position; finally the staged tile
+// goes out in digit order, every digit's run to its global offset (coalesced).
+__global__ void __launch_bounds__(TS_BLOCK) k_trip_scatter(const uint64_t* __restrict__ kin, const double* __restrict__ vin,
+                                                            uint64_t* __restrict__ kout, double* __restrict__ vout,
                                                             int64_t len, int shift, int64_t ntiles,
                                                             const int64_t* __restrict__ hist) {
-    __shared__ int64_t s_base[TS_RADIX];
+    extern __shared__ __align__(16) unsigned char ts_dyn[];
+    uint64_t* s_key = reinterpret_cast<uint64_t*>(ts_dyn);      // [TS_TILE]
+    double* s_val = reinterpret_cast<double*>(s_key + TS_TILE);  // [TS_TILE]
+    __shared__ int64_t s_gbase[TS_RADIX];  // global start of the tile's run of each digit
+    __shared__ int s_start[TS_RADIX];      // tile-local start of each digit
+    __shared__ int s_run[TS_RADIX];        // pairs of each digit staged so far
     __shared__ int s_w[TS_BLOCK / 32][TS_RADIX];
+    __shared__ int s_warp[TS_BLOCK / 32];
+    __shared__ int s_total;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    s_base[tid] = hist[int64_t(tid) * ntiles + blockIdx.x];
     const int64_t base = int64_t(blockIdx.x) * TS_TILE;
+    const int tn = int(len - base < TS_TILE ? len - base : TS_TILE);
+    s_gbase[tid] = hist[int64_t(tid) * ntiles + blockIdx.x];
+    s_run[tid] = 0;
+    s_start[tid] = 0;
+    __syncthreads();
+    uint64_t k[TS_ROUNDS];
+    double v[TS_ROUNDS];
+#pragma unroll
+    for (int r = 0; r < TS_ROUNDS; ++r) {
+        const int i = r * TS_BLOCK + tid;
+        k[r] = i < tn ? kin[base + i] : 0;
+        v[r] = i < tn ? vin[base + i] : 0.0;
+        if (i < tn) atomicAdd(&s_start[int((k[r] >> shift) & 0xff)], 1);
+    }
+    __syncthreads();
+    {  // tile-local digit starts
+        const int c = s_start[tid];
+        const int ex = block_exclusive_scan<TS_BLOCK>(c, s_warp, &s_total);
+        __syncthreads();
+        s_start[tid] = ex;
+    }
     const unsigned lt = (1u << lane) - 1u;
     for (int r = 0; r < TS_ROUNDS; ++r) {
 #pragma unroll
         for (int w = 0; w < TS_BLOCK / 32; ++w) s_w[w][tid] = 0;
         __syncthreads();
-        const int64_t i = base + r * TS_BLOCK + tid;
-        const bool valid = i < len;
-        uint64_t k = 0;
-        int64_t ix = 0;
-        int d = 0;
-        if (valid) {
-            k = kin[i];
-            ix = iin[i];
-            d = int((k >> shift) & 0xff);
-        }
+        const bool valid = r * TS_BLOCK + tid < tn;
+        const int d = valid ? int((k[r] >> shift) & 0xff) : 0;
         const unsigned peers = __match_any_sync(0xffffffffu, valid ? d : TS_RADIX + lane);
         const int rank = __popc(peers & lt);
         if (valid && rank == 0) s_w[warp][d] = __popc(peers);
         __syncthreads();
-        {  // thread `tid` owns digit tid: ordered exclusive offsets across warps
-            int64_t run = s_base[tid];
+        {  // thread `tid` owns digit tid: ordered offsets of the warps' groups in this round
+            int run = s_run[tid];
 #pragma unroll
             for (int w = 0; w < TS_BLOCK / 32; ++w) {
                 const int c = s_w[w][tid];
-                s_w[w][tid] = int(run - s_base[tid]);  // offset relative to the running base
+                s_w[w][tid] = run;
                 run += c;
             }
-            // keep the absolute base for this round in a register, publish the new base after use
-            __syncthreads();
-            if (valid) {
-                const int64_t dest = s_base[d] + s_w[warp][d] + rank;
-                kout[dest] = k;
-                iout[dest] = ix;
-            }
-            __syncthreads();
-            s_base[tid] = run;
+            s_run[tid] = run;
         }
         __syncthreads();
+        if (valid) {
+            const int lp = s_start[d] + s_w[warp][d] + rank;
+            s_key[lp] = k[r];
+            s_val[lp] = v[r];
+        }
+        __syncthreads();  // s_w is read above before the next round clears it
+    }
+    for (int p = tid; p < tn; p += TS_BLOCK) {
+        const uint64_t key = s_key[p];
+        const int d = int((key >> shift) & 0xff);
+        const int64_t dest = s_gbase[d] + (p - s_start[d]);
+        kout[dest] = key;
+        vout[dest] = s_val[p];
     }
 }
 
@@ -172,16 +206,16 @@ __global__ void k_trip_heads(const uint64_t* __restrict__ key, int64_t len, int*
 // ties in input order), then flag the position when the sum is nonzero.
 // keep_zeros (CscBuilder semantics, sparse.py:208-290): the sum starts from the run's first
 // value (`aa[pos] += v` after the first insertion stores v) and every position is stored.
-__global__ void k_trip_sums(const uint64_t* __restrict__ key, const int64_t* __restrict__ idx,
-                            const double* __restrict__ vals, int64_t len, int* __restrict__ keep,
+__global__ void k_trip_sums(const uint64_t* __restrict__ key, const double* __restrict__ vals, int64_t len,
+                            int* __restrict__ keep,
                             double* __restrict__ sums, fa_result* res, int keep_zeros) {
     for (int64_t i = blockIdx.x * int64_t(blockDim.x) + threadIdx.x; i < len; i += int64_t(gridDim.x) * blockDim.x) {
         const bool head = i == 0 || key[i] != key[i - 1];
         if (!head) { keep[i] = 0; continue; }
-        double s = keep_zeros ? vals[idx[i]] : 0.0;
+        double s = keep_zeros ? vals[i] : 0.0;
         int64_t j = keep_zeros ? i + 1 : i;
         while (j < len && key[j] == key[i]) {
-            s = __dadd_rn(s, vals[idx[j]]);
+            s = __dadd_rn(s, vals[j]);
             ++j;
         }
         sums[i] = s;
@@ -191,7 +225,7 @@ __global__ void k_trip_sums(const uint64_t* __restrict__ key, const int64_t* __r
             // count only positions with at least one nonzero input (the reference never sees
             // all-zero positions); diagnostic only
             bool any = false;
-            for (int64_t t = i; t < j; ++t) any |= vals[idx[t]] != 0.0;
+            for (int64_t t = i; t < j; ++t) any |= vals[t] != 0.0;
             if (any) atomicAdd(reinterpret_cast<unsigned long long*>(&res->dropped), 1ull);
         }
     }
@@ -269,14 +303,15 @@ extern "C" int fa_triplets_to_csc_ex(const int64_t* d_rows, const int64_t* d_col
         return FA_OK;
     }
     const int tb = 256;
-    k_trip_keys<<<grid_for(len, tb), tb, 0, st>>>(d_rows, d_cols, len, n_rows, n_cols, w.key0, w.idx0, d_res);
+    k_trip_keys<<<grid_for(len, tb), tb, 0, st>>>(d_rows, d_cols, d_vals, len, n_rows, n_cols, w.key0, w.val0, d_res);
     FA_LAUNCH_CHECK("k_trip_keys");
     // bits needed for codes in [0, n_rows*n_cols)
     const unsigned __int128 span = (unsigned __int128)n_rows * (unsigned __int128)n_cols;
     int bits = 0;
     while (bits < 64 && ((unsigned __int128)1 << bits) < span) ++bits;
     uint64_t *kin = w.key0, *kout = w.key1;
-    int64_t *iin = w.idx0, *iout = w.idx1;
+    double *vin = w.val0, *vout = w.val1;
+    FA_CUDA(cudaFuncSetAttribute(k_trip_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, int(TS_STAGE_BYTES)));
     for (int shift = 0; shift < bits; shift += 8) {
         k_trip_hist<<<dim3(unsigned(w.ntiles)), TS_BLOCK, 0, st>>>(kin, len, shift, w.ntiles, w.hist);
         FA_LAUNCH_CHECK("k_trip_hist");
@@ -286,19 +321,20 @@ extern "C" int fa_triplets_to_csc_ex(const int64_t* d_rows, const int64_t* d_col
         FA_CUDA(cudaMemsetAsync(w.ticket, 0, sizeof(unsigned long long), st));
         k_scan_i64_inplace<<<dim3(unsigned(stiles)), 256, 0, st>>>(w.hist, hn, w.status, w.ticket);
         FA_LAUNCH_CHECK("k_scan_i64_inplace");
-        k_trip_scatter<<<dim3(unsigned(w.ntiles)), TS_BLOCK, 0, st>>>(kin, iin, kout, iout, len, shift, w.ntiles, w.hist);
+        k_trip_scatter<<<dim3(unsigned(w.ntiles)), TS_BLOCK, TS_STAGE_BYTES, st>>>(kin, vin, kout, vout, len, shift,
+                                                                                   w.ntiles, w.hist);
         FA_LAUNCH_CHECK("k_trip_scatter");
         uint64_t* tk = kin; kin = kout; kout = tk;
-        int64_t* ti = iin; iin = iout; iout = ti;
+        double* tv = vin; vin = vout; vout = tv;
     }
-    // sums per run (values gathered through the permutation); reuse kout as f64 storage
+    // sums per run (the values travelled with their codes); kout is free f64 storage
     double* sums = reinterpret_cast<double*>(kout);
-    k_trip_sums<<<grid_for(len, tb), tb, 0, st>>>(kin, iin, d_vals, len, w.flag, sums, d_res,
+    k_trip_sums<<<grid_for(len, tb), tb, 0, st>>>(kin, vin, len, w.flag, sums, d_res,
                                                    (flags & FA_TRIPLETS_KEEP_ZEROS) ? 1 : 0);
     FA_LAUNCH_CHECK("k_trip_sums");
     int rc = scan_i32_flags(w.flag, w.pos, len, w, st);
     if (rc != FA_OK) return rc;
-    int64_t* colbuf = iout;
+    int64_t* colbuf = reinterpret_cast<int64_t*>(vout);
     k_trip_emit<<<grid_for(len, tb), tb, 0, st>>>(kin, sums, w.flag, w.pos, len, n_rows, d_rowidx, d_vals_out, colbuf);
     FA_LAUNCH_CHECK("k_trip_emit");
     k_trip_colptr<<<grid_for(n_cols + 1, tb), tb, 0, st>>>(colbuf, w.pos + len, n_cols, d_colptr);

@@ -2,7 +2,7 @@
 
 ``csc_from_triplets`` keeps Matlab ``sparse`` semantics (input zeros ignored, duplicates
 summed left to right in input order, exact-zero sums dropped, sparse.py:140-189) but runs
-on the GPU (fa_triplets_to_csc: stable LSD radix sort + sequential run sums).
+on the GPU (fa_triplets_to_csc: stable LSD radix sort of (code, value) pairs with shared-memory-staged tiles + sequential run sums).
 ``CscMatrix`` has the reference's immutable host interface (col_ptr/row_idx int64, values
 f64) and can also wrap a device CSR produced by ``assemble``; its host arrays are then
 materialised on first access.  ``CscBuilder`` — the deliberately quadratic insertion
