@@ -70,7 +70,6 @@ constexpr int ROWS_AU = 3, ROWS_AU_W = 3, ROWS_AU_E = 1;
 constexpr int ROWS_MINB_S = 5, CAPB_S = 832, ROWS_AU_S = 2;
 constexpr int MAXD = 8;            // incidences per row on the register fast path
 constexpr int PLOG0 = 10;          // log2 of the minimum part size (vertices)
-constexpr int MAX_PARTS = 8192;
 constexpr int PLAN_THREADS = 1024;
 constexpr int SORT_THREADS = 512;   // k_part_sort (2 blocks / SM, 64 registers)
 constexpr int PLACE_THREADS = 1024;  // k_part_hist / k_part_place block size
@@ -786,10 +785,10 @@ constexpr size_t rows_smem_bytes() {
     return KindTraits<KIND>::REC_BYTES;
 }
 
-// Gathered data of one incidence: neighbour coordinates / weights and the triangle area.
+// Gathered data of one incidence: neighbour coordinates, the triangle area, the W record.
 struct Gathered {
     double2 p1, p2;
-    double w1, w2, ar;
+    double ar;
     double4 wt;  // weighted mass: the triangle's W0, W1, W2 (k_tri_wt)
 };
 
@@ -798,7 +797,6 @@ __device__ __forceinline__ Gathered gather_incidence(const RowsArgs& A, unsigned
                                                      uint64_t pol) {
     Gathered g;
     g.p1 = g.p2 = make_double2(0.0, 0.0);
-    g.w1 = g.w2 = 0.0;
     g.ar = (KIND != FA_KIND_MASSW && A.areas) ? ld_keep_f64(A.areas + k, pol) : 0.0;
     if (KIND == FA_KIND_STIFF || KIND == FA_KIND_ELASTIC || !A.areas) {
         g.p1 = ld_keep_f64x2(A.q + n1, pol);
@@ -1129,7 +1127,6 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     __shared__ int64_t s_tile;
     __shared__ uint64_t s_prefix;
     __shared__ int64_t s_warp[NT / 32];
-    __shared__ int64_t s_total;
     __shared__ unsigned s_zeros;
     if (threadIdx.x == 0) s_zeros = 0;  // ordered before its atomics by next_tile's barrier
 
