@@ -1866,6 +1866,7 @@ static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* s
                       const double* wt_areas = nullptr, const double* wt_w = nullptr);
 
 extern "C" int fa_plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* stream) {
+    NvtxRange nv("fa_plan_build");
     return plan_build(p, d_me, d_res, stream, true);
 }
 
@@ -1971,6 +1972,9 @@ static int launch_tri_wt(fa_plan* p, const double* d_areas, const double* d_w, c
 extern "C" int fa_assemble(fa_plan* p, int kind, const double* d_q, const double* d_areas, const double* d_w,
                            double lam, double mu, int64_t* d_rowptr, int32_t* d_col, double* d_val, int64_t capacity,
                            fa_result* d_res, void* stream) {
+    static const char* const kNames[4] = {"fa_assemble mass", "fa_assemble massw", "fa_assemble stiff",
+                                          "fa_assemble elastic"};
+    NvtxRange nv(kind >= 0 && kind < 4 ? kNames[kind] : "fa_assemble");
     if (!p || !p->built) { set_error("fa_assemble: plan not built"); return FA_ERR_ARGUMENT; }
     if (!d_rowptr || !d_col || !d_val || !d_res) { set_error("fa_assemble: NULL output"); return FA_ERR_ARGUMENT; }
     if (kind < 0 || kind > 3) { set_error("unknown matrix kind %d", kind); return FA_ERR_ARGUMENT; }
@@ -2036,6 +2040,7 @@ extern "C" int fa_assemble_cold(fa_plan* p, const int32_t* d_me, int kind, const
                                 const double* d_w, double lam, double mu, int64_t* d_rowptr, int32_t* d_col,
                                 double* d_val, int64_t capacity, fa_result* d_build_result, fa_result* d_result,
                                 void* stream) {
+    NvtxRange nv("fa_assemble_cold");
     if (!p || !d_me || !d_build_result) { set_error("fa_assemble_cold: NULL argument"); return FA_ERR_ARGUMENT; }
     // weighted mass: the plan's histogram pass also writes the W records (k_tri_wt's work)
     const bool wt = kind == FA_KIND_MASSW && d_areas && d_w && p->nb > 0;

@@ -5,10 +5,19 @@
 #include <cstdint>
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 
 #include "../../include/femasm_b200.h"
 
 namespace fa {
+
+// NVTX range around a host entry point (visible in Nsight timelines; a no-op without a tool)
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 constexpr double AREA_EPS = 1e-300;  // mesh.py:27 (AREA_EPS)
 

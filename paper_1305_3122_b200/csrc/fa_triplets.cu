@@ -288,6 +288,7 @@ extern "C" int fa_triplets_to_csc(const int64_t* d_rows, const int64_t* d_cols, 
 extern "C" int fa_triplets_to_csc_ex(const int64_t* d_rows, const int64_t* d_cols, const double* d_vals, int64_t len,
                                      int64_t n_rows, int64_t n_cols, int flags, int64_t* d_colptr, int64_t* d_rowidx,
                                      double* d_vals_out, void* d_ws, size_t ws_bytes, fa_result* d_res, void* stream) {
+    NvtxRange nv("fa_triplets_to_csc");
     if (len < 0 || n_rows < 1 || n_cols < 1) { set_error("matrix dimensions must be positive"); return FA_ERR_ARGUMENT; }
     if (!d_colptr || !d_res || !d_ws || (len > 0 && (!d_rows || !d_cols || !d_vals || !d_rowidx || !d_vals_out))) {
         set_error("fa_triplets_to_csc: NULL argument"); return FA_ERR_ARGUMENT;
