@@ -35,13 +35,24 @@ def _stale() -> bool:
     return any(p.stat().st_mtime > mtime for p in deps if p.exists())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not _stale():
-        return OUT
+# checked build (device-side bounds and spin-limit checks, FA_DCHECK in csrc/fa_common.cuh):
+# a test artefact loaded by tests/test_checked_build.py, never by the package
+OUT_CHECKED = PKG_DIR / "libfemasm_b200_checked.so"
+
+
+def _stale_for(out: Path) -> bool:
+    if not out.exists():
+        return True
+    mtime = out.stat().st_mtime
+    deps = list(CSRC.glob("*.cu")) + list(CSRC.glob("*.cuh")) + [PKG_DIR.parent / "include" / "femasm_b200.h"]
+    return any(p.stat().st_mtime > mtime for p in deps if p.exists())
+
+
+def _nvcc(out: Path, extra: list[str], verbose: bool) -> str:
     cmd = [
         nvcc_path(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-fmad=false",
-        "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v",
-        "-o", str(OUT) + ".tmp", *[str(CSRC / s) for s in SOURCES],
+        "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v", *extra,
+        "-o", str(out) + ".tmp", *[str(CSRC / s) for s in SOURCES],
     ]
     proc = subprocess.run(cmd, capture_output=True, text=True)
     if proc.returncode != 0:
@@ -49,10 +60,24 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError(f"nvcc failed ({proc.returncode})")
     if verbose:
         sys.stderr.write(proc.stderr)
-    os.replace(str(OUT) + ".tmp", OUT)
-    (PKG_DIR / "build_ptxas.log").write_text(proc.stderr)
+    os.replace(str(out) + ".tmp", out)
+    return proc.stderr
+
+
+def build(force: bool = False, verbose: bool = False) -> Path:
+    if not force and not _stale():
+        return OUT
+    (PKG_DIR / "build_ptxas.log").write_text(_nvcc(OUT, [], verbose))
     return OUT
+
+
+def build_checked(force: bool = False) -> Path:
+    if force or _stale_for(OUT_CHECKED):
+        _nvcc(OUT_CHECKED, ["-DFA_CHECKED"], False)
+    return OUT_CHECKED
 
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    if "--checked" in sys.argv:
+        print(build_checked(force="--force" in sys.argv))

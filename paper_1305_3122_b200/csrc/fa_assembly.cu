@@ -422,6 +422,7 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
         for (int j = 0; j < 3 * TPT; ++j) {
             if (part[j] != 0xffffffffu) {
                 const unsigned pos = s_lst[part[j]] + rank[j];
+                FA_DCHECK(pos < unsigned(RI), "placement staging index");
                 s_stage[pos] = rec[j];
                 s_part[pos] = (unsigned short)part[j];
             }
@@ -432,6 +433,7 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
             const unsigned p = s_part[i];
             const unsigned g = s_gb[p] + (unsigned(i) - s_lst[p]);
             const uint4 r = s_stage[i];
+            FA_DCHECK(int64_t(g) < 3 * P.nme, "placement record index");
             asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(P.rec + g), "r"(r.x),
                          "r"(r.y), "r"(r.z), "r"(r.w)
                          : "memory");
@@ -514,6 +516,7 @@ __global__ void __launch_bounds__(SPLIT_THREADS, SPLIT_MINB)
             if (f[u] == 0xffffffffu) continue;
             const unsigned l = f[u] - fb;
             const unsigned pos = s_lst[l] + rank[u];
+            FA_DCHECK(pos < unsigned(RI), "split staging index");
             s_stage[pos] = r[u];
             s_fp[pos] = (unsigned short)l;
         }
@@ -653,6 +656,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_cons
         for (int u = 0; u < RU; ++u) {
             if (i0 + u * SORT_THREADS < n) {
                 const unsigned pos = atomicAdd(&s_cur[(r[u].y >> 2) & unsigned(PV - 1)], 1u);
+                FA_DCHECK(pos < n, "part sort position");
                 key[pos] = (r[u].x << 2) | (r[u].y & 3u);
                 n1[pos] = r[u].z;
                 n2[pos] = r[u].w;
@@ -698,6 +702,7 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_cons
         __syncthreads();
         for (unsigned i = tid; i < n; i += SORT_THREADS) {
             const unsigned j = s_src[i];
+            FA_DCHECK(j < n, "part sort source slot");
             P.skey[off + i] = key[j];
             P.sn1[off + i] = n1[j];
             P.sn2[off + i] = n2[j];
@@ -1170,7 +1175,10 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     }
     __syncthreads();
     for (int vl = tid; vl < nvb && !overflow; vl += NT)
-        for (int j = s_vst[vl]; j < s_vst[vl + 1]; ++j) s_own[j] = (unsigned char)vl;
+        for (int j = s_vst[vl]; j < s_vst[vl + 1]; ++j) {
+            FA_DCHECK(j < CAP, "row bucket slot");
+            s_own[j] = (unsigned char)vl;
+        }
     // ---- s) the bucket's plan entries -> shared memory (coalesced)
     if constexpr (!EARLY_LOAD) load_entries();
 #pragma unroll
@@ -1268,6 +1276,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         const bool staged = !any_slow && total <= CAP;
         double* sv = reinterpret_cast<double*>(R.n1);    // [CAP], spans n1 and n2
         int32_t* sc = reinterpret_cast<int32_t*>(R.ka);  // [CAP]
+        FA_DCHECK(!staged || !fast || excl + count <= total, "row segment inside the bucket's");
         if (staged && fast) zeros = walk_row<KIND, false>(R, sk, start, deg, vv, dpos, sc + excl, sv + excl, 0);
         base = lookback_wait(A.status, b, uint64_t(total), &s_prefix);  // ends with a barrier
         if (active) st_stream_i64(A.rowptr + r, int64_t(base) + excl, pol_first);
@@ -1379,6 +1388,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
 #pragma unroll
                     for (int t = 0; t < NV; ++t) {
                         if (!EARLY && run_val[j][t] == 0.0) continue;
+                        FA_DCHECK(o < TR::STAGE, "row staging index");
                         st_col[o] = NV == 1 ? int(prev) : int(2 * prev + t);
                         st_val[o] = run_val[j][t];
                         ++o;
@@ -1388,6 +1398,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
 #pragma unroll
                     for (int t = 0; t < NV; ++t) {
                         if (!EARLY && dsum[t] == 0.0) continue;
+                        FA_DCHECK(o < TR::STAGE, "row staging index");
                         st_col[o] = NV == 1 ? int(vv) : int(2 * vv + t);
                         st_val[o] = dsum[t];
                         ++o;
@@ -1521,7 +1532,8 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const unsigned long lon
         }
     }
     if (tid == 0)
-        while (atomicAdd(scan_ready, 0u) == 0u) __nanosleep(256);
+        for (unsigned spins = 0; atomicAdd(scan_ready, 0u) == 0u; __nanosleep(256))
+            FA_DCHECK(++spins < FA_SPIN_LIMIT, "compaction scan wait");
     __syncthreads();
     __threadfence();
     while (true) {  // persistent: buckets in ticket order
@@ -1559,7 +1571,8 @@ __global__ void __launch_bounds__(CMP_THREADS) k_compact(const unsigned long lon
     if (tid == 0) {
         for (int64_t bp = b - 1; bp >= 0; --bp) {
             if (bsym[bp] + blen[bp] <= D) break;
-            while (atomicAdd(&read_done[bp], 0u) == 0u) __nanosleep(64);
+            for (unsigned spins = 0; atomicAdd(&read_done[bp], 0u) == 0u; __nanosleep(64))
+                FA_DCHECK(++spins < FA_SPIN_LIMIT, "compaction overlap wait");
         }
         __threadfence();
     }

@@ -11,6 +11,26 @@
 
 namespace fa {
 
+// Device-side checks of the checked build (libfemasm_b200_checked.so, -DFA_CHECKED): shared-
+// and global-memory indices against their bounds and spin-wait limits, trapping with the
+// location.  This pool refuses compute-sanitizer; tests/test_checked_build.py runs the kernels
+// under these checks instead.  Compiled out of the product library.
+#ifdef FA_CHECKED
+#define FA_DCHECK(cond, what)                                                              \
+    do {                                                                                   \
+        if (!(cond)) {                                                                     \
+            printf("FA_CHECKED failure %s:%d block %d thread %d: %s\n", __FILE__, __LINE__, \
+                   int(blockIdx.x), int(threadIdx.x), what);                               \
+            __trap();                                                                      \
+        }                                                                                  \
+    } while (0)
+#else
+#define FA_DCHECK(cond, what) \
+    do {                      \
+    } while (0)
+#endif
+constexpr unsigned FA_SPIN_LIMIT = 1u << 24;  // checked build: a wait this long is a deadlock
+
 // NVTX range around a host entry point (visible in Nsight timelines; a no-op without a tool)
 struct NvtxRange {
     explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
@@ -277,7 +297,9 @@ __device__ __forceinline__ void lookback_resolve(uint64_t* status, int64_t tile,
             uint64_t excl = 0;
             int64_t pred = tile - 1;
             unsigned backoff = 32;  // ns; doubles while predecessors are still empty (frees issue slots)
+            unsigned spins = 0;
             while (true) {
+                FA_DCHECK(++spins < FA_SPIN_LIMIT, "look-back wait");
                 int64_t t = pred - lane;
                 uint64_t w = t >= 0 ? ld_volatile_u64(&status[t]) : lb_pack(2, 0);
                 uint64_t flag = w >> 62;
