@@ -162,6 +162,10 @@ class CscMatrix:
         import torch
 
         ptr, idx, vals = self.device_arrays()
+        # torch wants one index dtype: the int32 column ids are handed over as they are (zero
+        # copy) and the row pointers narrowed (n+1 entries instead of nnz) whenever nnz fits
+        if idx.dtype == torch.int32 and int(self.nnz) < 2**31:
+            return torch.sparse_csr_tensor(ptr.to(torch.int32), idx, vals, size=(self.n_cols, self.n_rows))
         return torch.sparse_csr_tensor(ptr, idx.to(torch.int64), vals, size=(self.n_cols, self.n_rows))
 
     def __repr__(self) -> str:

@@ -246,6 +246,8 @@ def test_paper_entry_points_and_handoff(golden):
     assert np.array_equal(sp.toarray(), m.to_dense())
     t = m.to_torch_sparse_csr()
     assert np.array_equal(t.to_dense().cpu().numpy(), m.to_dense())
+    # zero-copy hand-off: the CSR column ids are the device array itself
+    assert t.col_indices().data_ptr() == m.device_arrays()[1].data_ptr()
 
 
 def test_mesh_text_roundtrip_and_generators(golden, tmp_path):
