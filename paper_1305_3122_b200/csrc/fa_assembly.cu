@@ -1753,6 +1753,7 @@ struct fa_plan {
     unsigned long long* bshift;  // nb
     unsigned* read_done;      // nb (k_compact)
     int64_t ninc;             // -1 until read back
+    cudaStream_t build_stream;  // stream of the last build (fa_plan_capacity reads its counts there)
     bool built;
     // fa_assemble_cold: W records written by the plan's histogram pass, consumed once
     const void* wt_key[3];    // (me, areas, w) the prepared W records belong to; consumed once
@@ -1894,6 +1895,7 @@ static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* s
     cudaStream_t st = as_stream(stream);
     p->ninc = -1;
     p->built = true;
+    p->build_stream = st;
     if (p->nb == 0) {
         k_result_reset<<<1, 32, 0, st>>>(d_res);
         return FA_OK;
@@ -1968,7 +1970,11 @@ extern "C" int fa_plan_capacity(fa_plan* p, int kind, int64_t* capacity) {
             p->ninc = 3 * p->nme;  // every corner is owned
         } else {
             unsigned total = 0;
-            FA_CUDA(cudaMemcpy(&total, p->part_off + p->nparts, sizeof(unsigned), cudaMemcpyDeviceToHost));
+            // ordered after the build on its own stream (a non-blocking stream does not
+            // synchronise with the legacy default stream)
+            FA_CUDA(cudaMemcpyAsync(&total, p->part_off + p->nparts, sizeof(unsigned), cudaMemcpyDeviceToHost,
+                                    p->build_stream));
+            FA_CUDA(cudaStreamSynchronize(p->build_stream));
             p->ninc = int64_t(total);
         }
     }

@@ -494,3 +494,23 @@ def test_reused_plan_with_changed_values(kind):
         wd = torch.from_numpy(w).to(dev)
         rowptr, col, val, r = plan.assemble(kind, q=q, areas=a, w=wd, lam=lam, mu=mu)
         assert_same_csc((rowptr.cpu().numpy(), col.cpu().numpy(), val.cpu().numpy()), ref, f"{kind} call {it}")
+
+
+def test_row_block_capacity_after_build_on_a_side_stream():
+    """fa_plan_capacity reads the row block's incidence count on the stream the build ran on
+    (a non-blocking stream is not ordered with the legacy default stream)."""
+    import torch
+
+    sm = seeded_square_mesh(64, 3)
+    me = torch.from_numpy(sm.connectivity.astype(np.int32)).cuda()
+    ref = fa.AssemblyPlan(sm.nme, sm.nq, 500, 2500)
+    ref.build(me)
+    torch.cuda.synchronize()
+    want = ref.capacity("stiff")
+    side = torch.cuda.Stream()
+    for _ in range(3):
+        plan = fa.AssemblyPlan(sm.nme, sm.nq, 500, 2500)
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            plan.build(me, stream=side)
+            assert plan.capacity("stiff") == want
