@@ -88,7 +88,7 @@ constexpr int SPLIT_THREADS = 512;
 constexpr int SPLIT_RI = 4096;      // records per k_part_split round
 constexpr int SPLIT_MINB = 2;       // k_part_split blocks per SM
 constexpr int SPLIT2_LOCAL = SPLIT_THREADS;  // fine parts a k_part_split round ranks in shared memory
-constexpr int SORT_CAP = 7680;     // part incidences sorted in shared memory (2 blocks / SM)
+constexpr int SORT_CAP = 6912;     // part incidences sorted in shared memory (6.75 per vertex; 2 blocks / SM)
 
 // Resets the result block and zeroes the counters the following kernels accumulate into
 // (grid-stride; replaces separate memsets).
@@ -573,6 +573,39 @@ __device__ void sort_incidences(unsigned* key, unsigned* n1, unsigned* n2, int d
     }
 }
 
+// Sort the slots idx[0..d) by key[slot] (unique keys): insertion sort for short lists, heapsort
+// beyond.
+__device__ void sort_slots(unsigned short* idx, const unsigned* key, int d) {
+    if (d <= 32) {
+        for (int i = 1; i < d; ++i) {
+            const unsigned short s = idx[i];
+            const unsigned x = key[s];
+            int j = i - 1;
+            while (j >= 0 && key[idx[j]] > x) {
+                idx[j + 1] = idx[j];
+                --j;
+            }
+            idx[j + 1] = s;
+        }
+        return;
+    }
+    auto sift = [&](int root, int end) {
+        while (true) {
+            int child = 2 * root + 1;
+            if (child >= end) break;
+            if (child + 1 < end && key[idx[child + 1]] > key[idx[child]]) ++child;
+            if (key[idx[root]] >= key[idx[child]]) break;
+            const unsigned short t = idx[root]; idx[root] = idx[child]; idx[child] = t;
+            root = child;
+        }
+    };
+    for (int i = d / 2 - 1; i >= 0; --i) sift(i, d);
+    for (int end = d - 1; end > 0; --end) {
+        const unsigned short t = idx[0]; idx[0] = idx[end]; idx[end] = t;
+        sift(0, end);
+    }
+}
+
 // 8 keys ascending (19 comparators, verified by the 0-1 principle)
 __device__ __forceinline__ void sort8(unsigned (&k)[8]) {
     auto cx = [](unsigned& x, unsigned& y) {
@@ -608,14 +641,48 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_cons
     const uint64_t pol = l2_evict_first_policy();
     for (int i = tid; i < PV; i += SORT_THREADS) s_cur[i] = 0;
     __syncthreads();
-    {  // vertex counts: eight records in flight per thread
+    unsigned* key = fast ? s_dyn + PV : P.skey + off;
+    unsigned* n1 = fast ? s_dyn + PV + SORT_CAP : P.sn1 + off;
+    unsigned* n2 = fast ? s_dyn + PV + 2 * SORT_CAP : P.sn2 + off;
+    // fast: [SORT_CAP] each.  s_src: vertex of the record in arrival slot i (until the records are
+    // ranked), then the source slot of every sorted position; s_grp: arrival slots grouped by vertex
+    unsigned short* s_src = reinterpret_cast<unsigned short*>(s_dyn + PV + 3 * SORT_CAP);
+    unsigned short* s_grp = s_src + SORT_CAP;
+    constexpr int RU = 6;  // records in flight per thread (C5 sort 3.50 -> 3.37 ms against four)
+    if (fast) {
+        // the part's records read once: (key, n1, n2, vertex) into shared memory in arrival order
+        // (conflict-free stores) while the vertices are counted
+        for (unsigned i0 = tid; i0 < n; i0 += RU * SORT_THREADS) {
+            uint4 r[RU];
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+                const unsigned i = i0 + u * SORT_THREADS;
+                if (i < n)
+                    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                                 : "=r"(r[u].x), "=r"(r[u].y), "=r"(r[u].z), "=r"(r[u].w)
+                                 : "l"(P.rec + off + i), "l"(pol));
+            }
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+                const unsigned i = i0 + u * SORT_THREADS;
+                if (i < n) {
+                    const unsigned vl = (r[u].y >> 2) & unsigned(PV - 1);
+                    key[i] = (r[u].x << 2) | (r[u].y & 3u);
+                    n1[i] = r[u].z;
+                    n2[i] = r[u].w;
+                    s_src[i] = (unsigned short)vl;
+                    atomicAdd(&s_cur[vl], 1u);
+                }
+            }
+        }
+    } else {  // vertex counts: eight records in flight per thread
         const unsigned* ry = reinterpret_cast<const unsigned*>(P.rec + off) + 1;  // .y fields
         for (unsigned i0 = tid; i0 < n; i0 += 8 * SORT_THREADS) {
             unsigned y[8];
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 const unsigned i = i0 + u * SORT_THREADS;
-                y[u] = i < n ? ry[4 * size_t(i)] : 0xffffffffu;  // L1-allocating: the record pass below hits
+                y[u] = i < n ? ry[4 * size_t(i)] : 0xffffffffu;
             }
 #pragma unroll
             for (int u = 0; u < 8; ++u)
@@ -637,29 +704,32 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_cons
     }
     if (p == P.nparts - 1 && tid == 0) P.ivptr[nv] = off + n;
     __syncthreads();
-    unsigned* key = fast ? s_dyn + PV : P.skey + off;
-    unsigned* n1 = fast ? s_dyn + PV + SORT_CAP : P.sn1 + off;
-    unsigned* n2 = fast ? s_dyn + PV + 2 * SORT_CAP : P.sn2 + off;
-    unsigned short* s_src = reinterpret_cast<unsigned short*>(s_dyn + PV + 3 * SORT_CAP);  // fast: [SORT_CAP]
-    constexpr int RU = 6;  // records in flight per thread (C5 sort 3.50 -> 3.37 ms against four)
-    for (unsigned i0 = tid; i0 < n; i0 += RU * SORT_THREADS) {
-        uint4 r[RU];
-#pragma unroll
-        for (int u = 0; u < RU; ++u) {
-            const unsigned i = i0 + u * SORT_THREADS;
-            if (i < n)
-                asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
-                             : "=r"(r[u].x), "=r"(r[u].y), "=r"(r[u].z), "=r"(r[u].w)
-                             : "l"(P.rec + off + i), "l"(pol));
+    if (fast) {  // arrival slots grouped by vertex (order inside a vertex's list is arbitrary)
+        for (unsigned i = tid; i < n; i += SORT_THREADS) {
+            const unsigned pos = atomicAdd(&s_cur[s_src[i]], 1u);
+            FA_DCHECK(pos < n, "part sort position");
+            s_grp[pos] = (unsigned short)i;
         }
+    } else {
+        for (unsigned i0 = tid; i0 < n; i0 += RU * SORT_THREADS) {
+            uint4 r[RU];
 #pragma unroll
-        for (int u = 0; u < RU; ++u) {
-            if (i0 + u * SORT_THREADS < n) {
-                const unsigned pos = atomicAdd(&s_cur[(r[u].y >> 2) & unsigned(PV - 1)], 1u);
-                FA_DCHECK(pos < n, "part sort position");
-                key[pos] = (r[u].x << 2) | (r[u].y & 3u);
-                n1[pos] = r[u].z;
-                n2[pos] = r[u].w;
+            for (int u = 0; u < RU; ++u) {
+                const unsigned i = i0 + u * SORT_THREADS;
+                if (i < n)
+                    asm volatile("ld.global.L1::no_allocate.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                                 : "=r"(r[u].x), "=r"(r[u].y), "=r"(r[u].z), "=r"(r[u].w)
+                                 : "l"(P.rec + off + i), "l"(pol));
+            }
+#pragma unroll
+            for (int u = 0; u < RU; ++u) {
+                if (i0 + u * SORT_THREADS < n) {
+                    const unsigned pos = atomicAdd(&s_cur[(r[u].y >> 2) & unsigned(PV - 1)], 1u);
+                    FA_DCHECK(pos < n, "part sort position");
+                    key[pos] = (r[u].x << 2) | (r[u].y & 3u);
+                    n1[pos] = r[u].z;
+                    n2[pos] = r[u].w;
+                }
             }
         }
     }
@@ -676,27 +746,27 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_cons
             // 19-comparator network: the sorted position's source slot is in the low bits
             unsigned kk[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) kk[j] = j < int(d) ? (key[st + j] << 3) | unsigned(j) : 0xffffffffu;
+            for (int j = 0; j < 8; ++j) kk[j] = j < int(d) ? (key[s_grp[st + j]] << 3) | unsigned(j) : 0xffffffffu;
             sort8(kk);
 #pragma unroll
             for (int r = 0; r < 8; ++r)
-                if (r < int(d)) s_src[st + r] = (unsigned short)(st + (kk[r] & 7u));
+                if (r < int(d)) s_src[st + r] = s_grp[st + (kk[r] & 7u)];
         } else if (d <= 8) {
             unsigned kk[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) kk[j] = j < int(d) ? key[st + j] : 0xffffffffu;
+            for (int j = 0; j < 8; ++j) kk[j] = j < int(d) ? key[s_grp[st + j]] : 0xffffffffu;
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
                 if (i < int(d)) {
                     unsigned r = 0;
 #pragma unroll
                     for (int j = 0; j < 8; ++j) r += kk[j] < kk[i] ? 1u : 0u;
-                    s_src[st + r] = (unsigned short)(st + i);
+                    s_src[st + r] = s_grp[st + i];
                 }
             }
         } else {
-            sort_incidences(key + st, n1 + st, n2 + st, int(d));
-            for (unsigned i = 0; i < d; ++i) s_src[st + i] = (unsigned short)(st + i);
+            sort_slots(s_grp + st, key, int(d));
+            for (unsigned i = 0; i < d; ++i) s_src[st + i] = s_grp[st + i];
         }
         }
         __syncthreads();
@@ -1777,7 +1847,7 @@ static size_t place_smem_bytes(int nparts) {
 static size_t sort_smem_bytes(int plog) {
     const size_t pv = size_t(1) << plog;
     return sizeof(unsigned) * pv +
-           (pv == (size_t(1) << PLOG0) ? (sizeof(unsigned) * 3 + sizeof(unsigned short)) * SORT_CAP : 0);  // k_part_sort
+           (pv == (size_t(1) << PLOG0) ? (sizeof(unsigned) * 3 + sizeof(unsigned short) * 2) * SORT_CAP : 0);  // k_part_sort
 }
 
 extern "C" int fa_plan_create(fa_plan** out, int64_t nme, int64_t nq, int64_t row_begin, int64_t row_end) {
