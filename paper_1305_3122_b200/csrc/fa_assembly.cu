@@ -938,9 +938,9 @@ __device__ __forceinline__ void incidence_values(const RowsArgs& A, unsigned k, 
         const double2 eo = dsub2(g.p1, g.p2), e1 = dsub2(g.p2, own_p), e2 = dsub2(own_p, g.p1);
         // three true divisions by a4 = 4*area sharing one correctly rounded reciprocal (div_by)
         const DivBy d4 = div_prepare(FMUL(4.0, ar));
-        out[0] = div_by(d4, FADD(FADD(0.0, FMUL(eo.x, eo.x)), FMUL(eo.y, eo.y)));
-        out[1] = div_by(d4, FADD(FADD(0.0, FMUL(eo.x, e1.x)), FMUL(eo.y, e1.y)));
-        out[2] = div_by(d4, FADD(FADD(0.0, FMUL(eo.x, e2.x)), FMUL(eo.y, e2.y)));
+        div_by3(d4, FADD(FADD(0.0, FMUL(eo.x, eo.x)), FMUL(eo.y, eo.y)),
+                FADD(FADD(0.0, FMUL(eo.x, e1.x)), FMUL(eo.y, e1.y)),
+                FADD(FADD(0.0, FMUL(eo.x, e2.x)), FMUL(eo.y, e2.y)), out[0], out[1], out[2]);
     } else {
         // gradients of the own corner and the two neighbours from the edges opposite them (the
         // reference's u, v, w in local order: same operands, same bits, assembly.py:195-211)

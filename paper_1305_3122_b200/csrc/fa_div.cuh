@@ -132,9 +132,14 @@ __device__ __forceinline__ double ddiv(double x, double y) {
 }
 
 // Several quotients x_i / y with one divisor (the stiffness row's three entries share 4*area):
-// r = RN(1/y) once (a full correctly rounded division), then each quotient by ddiv_rcp's two
-// residual corrections (Markstein: faithful q + RN(1/y) give RN(x/y)).  Operands, 1/y or the
-// quotient outside the safe exponent range take ddiv for that quotient.
+// r = RN(1/y) once, then each quotient by ddiv_rcp's two residual corrections (Markstein:
+// faithful q + RN(1/y) give RN(x/y)).  Operands, 1/y or the quotient outside the safe exponent
+// range take ddiv for that quotient.
+//
+// RN(1/y) for a positive y inside the safe exponent range: two Newton steps from rcp.approx
+// leave r within an ulp of 1/y, and one more step r + r * (1 - y r) with the exact fma residual
+// is then the correctly rounded reciprocal unless y's significand is all ones (Markstein's
+// reciprocal theorem) - that divisor, like zero, negative or extreme ones, takes ddiv.
 struct DivBy {
     double y, r;
     int ey;
@@ -142,10 +147,24 @@ struct DivBy {
 };
 __device__ __forceinline__ DivBy div_prepare(double y) {
     DivBy d;
+    const uint64_t by = __double_as_longlong(y);
     d.y = y;
-    d.ey = int((__double_as_longlong(y) >> 52) & 0x7ff) - 1023;
-    d.ok = d.ey >= -960 && d.ey <= 960;
-    d.r = d.ok ? ddiv(1.0, y) : 0.0;
+    d.ey = int((by >> 52) & 0x7ff) - 1023;
+    const bool plain = unsigned(d.ey + 960) <= 1920u && int64_t(by) > 0 &&
+                       (by & 0xfffffffffffffull) != 0xfffffffffffffull;
+    d.ok = unsigned(d.ey + 960) <= 1920u;
+    if (plain) {
+        double r;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(y));
+        double e = __fma_rn(-y, r, 1.0);
+        r = __fma_rn(e, r, r);
+        e = __fma_rn(-y, r, 1.0);
+        r = __fma_rn(e, r, r);
+        e = __fma_rn(-y, r, 1.0);
+        d.r = __fma_rn(e, r, r);
+    } else {
+        d.r = d.ok ? ddiv(1.0, y) : 0.0;
+    }
     return d;
 }
 __device__ __forceinline__ double div_by(const DivBy& d, double x) {
@@ -154,6 +173,27 @@ __device__ __forceinline__ double div_by(const DivBy& d, double x) {
     double q = __dmul_rn(x, d.r);
     q = __fma_rn(__fma_rn(-q, d.y, x), d.r, q);
     return __fma_rn(__fma_rn(-q, d.y, x), d.r, q);
+}
+// Three quotients by the same divisor with one range check for all (the largest and the
+// smallest numerator exponent bound the others); any operand outside takes div_by's path.
+__device__ __forceinline__ void div_by3(const DivBy& d, double x0, double x1, double x2, double& q0, double& q1,
+                                        double& q2) {
+    const int e0 = int((__double_as_longlong(x0) >> 52) & 0x7ff), e1 = int((__double_as_longlong(x1) >> 52) & 0x7ff),
+              e2 = int((__double_as_longlong(x2) >> 52) & 0x7ff);
+    const int lo = min(e0, min(e1, e2)) - 1023, hi = max(e0, max(e1, e2)) - 1023;
+    if (d.ok && lo >= -960 && hi <= 960 && lo - d.ey >= -960 && hi - d.ey <= 960) {
+        double a = __dmul_rn(x0, d.r), b = __dmul_rn(x1, d.r), c = __dmul_rn(x2, d.r);
+        a = __fma_rn(__fma_rn(-a, d.y, x0), d.r, a);
+        b = __fma_rn(__fma_rn(-b, d.y, x1), d.r, b);
+        c = __fma_rn(__fma_rn(-c, d.y, x2), d.r, c);
+        q0 = __fma_rn(__fma_rn(-a, d.y, x0), d.r, a);
+        q1 = __fma_rn(__fma_rn(-b, d.y, x1), d.r, b);
+        q2 = __fma_rn(__fma_rn(-c, d.y, x2), d.r, c);
+    } else {
+        q0 = div_by(d, x0);
+        q1 = div_by(d, x1);
+        q2 = div_by(d, x2);
+    }
 }
 
 }  // namespace fa

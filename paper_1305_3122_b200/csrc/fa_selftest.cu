@@ -58,6 +58,40 @@ __global__ void k_selftest_div(int64_t n, uint64_t seed, unsigned long long* bad
                 }
             }
         }
+        // the same three at a time (div_by3), also for divisors whose significand is all ones or
+        // just below (the reciprocal's exceptional case) and for plain positive divisors
+        {
+            const uint64_t hs = splitmix64(h + 41);
+            const double ya = __longlong_as_double((uint64_t(1 + (hs >> 40) % 2046) << 52) |
+                                                   (0xfffffffffffffull - ((hs >> 8) & 3ull)));
+            const double yb = __longlong_as_double((uint64_t(1023 - 40 + (hs >> 30) % 80) << 52) | (splitmix64(hs) >> 12));
+            const double ys3[3] = {y, ya, yb};
+            const double xs[3] = {x, gen_operand(splitmix64(h + 29)), 1.0 + double(hs >> 11) * 0x1.0p-53};
+#pragma unroll
+            for (int t = 0; t < 3; ++t) {
+                const DivBy d = div_prepare(ys3[t]);
+                double m[3];
+                div_by3(d, xs[0], xs[1], xs[2], m[0], m[1], m[2]);
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    const double r3 = __ddiv_rn(xs[j], ys3[t]);
+                    if (!(m[j] != m[j] && r3 != r3) && __double_as_longlong(m[j]) != __double_as_longlong(r3)) {
+                        if (atomicAdd(bad, 1ull) == 0) {
+                            first[0] = xs[j]; first[1] = ys3[t]; first[2] = m[j]; first[3] = r3;
+                        }
+                    }
+                }
+                // the reciprocal itself
+                if (d.ok) {
+                    const double rr = __ddiv_rn(1.0, ys3[t]);
+                    if (!(d.r != d.r && rr != rr) && __double_as_longlong(d.r) != __double_as_longlong(rr)) {
+                        if (atomicAdd(bad, 1ull) == 0) {
+                            first[0] = 1.0; first[1] = ys3[t]; first[2] = d.r; first[3] = rr;
+                        }
+                    }
+                }
+            }
+        }
         // constant divisors of the mass formulas (x only: y fixed)
         const double ys[3] = {6.0, 12.0, 30.0}, rs[3] = {FA_RCP6_, FA_RCP12_, FA_RCP30_};
 #pragma unroll
