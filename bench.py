@@ -81,7 +81,7 @@ def parse_args():
     ap.add_argument("--config", default=DEFAULT_CONFIG)
     ap.add_argument("--seed", type=int, default=0)
     ap.add_argument("--cpu-baseline-runs", type=int, default=2, help="timed runs of the 1-core CPU baseline (0: skip)")
-    ap.add_argument("--e2e-steps", type=int, default=6)
+    ap.add_argument("--e2e-steps", type=int, default=16)
     ap.add_argument("--graph", type=int, default=1, help="replay each step as a captured CUDA graph (N=1)")
     ap.add_argument("--verify", type=int, default=1, help="hash the last step's CSR against femasm's digests")
     ap.add_argument("--ref-budget-s", type=float, default=150.0,
