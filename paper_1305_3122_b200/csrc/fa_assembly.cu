@@ -43,6 +43,7 @@
 //                    sparse.py:177-179): removes those entries in place, bucket by bucket.
 // Rows of degree > MAXD (and every row of a bucket whose incidences exceed CAPB) use an
 // O(d^2) general path with the same summation order.
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 #include <new>
@@ -141,7 +142,8 @@ struct PlanArgs {
 };
 
 // a triangle takes part only with three in-range, pairwise distinct vertex ids
-__device__ __forceinline__ bool tri_ids_valid(int c0, int c1, int c2, int64_t nq) {
+// (vertex counts stay below 2^28, fa_plan_create: every comparison here and in the plan kernels is 32 bit)
+__device__ __forceinline__ bool tri_ids_valid(int c0, int c1, int c2, unsigned nq) {
     return unsigned(c0) < nq && unsigned(c1) < nq && unsigned(c2) < nq && c0 != c1 && c1 != c2 && c0 != c2;
 }
 
@@ -170,12 +172,12 @@ __device__ __noinline__ void hist_tri_wt(const PlanArgs& P, int64_t k0, int64_t 
         for (int u = 0; u < U; ++u) {
             bool any = false;
 #pragma unroll
-            for (int a = 0; a < 3; ++a) any |= c[u][a] >= P.v0 && c[u][a] < P.v1;
+            for (int a = 0; a < 3; ++a) any |= unsigned(c[u][a]) - unsigned(P.v0) < unsigned(P.v1 - P.v0);
             own[u] = k0u + u * PLACE_THREADS < k1 && any;
             if (own[u])
 #pragma unroll
                 for (int a = 0; a < 3; ++a)  // out-of-range ids (reported by the histogram) read nothing
-                    wc[u][a] = unsigned(c[u][a]) < P.nq ? ld_keep_f64(P.wt_w + c[u][a], keep) : 0.0;
+                    wc[u][a] = unsigned(c[u][a]) < unsigned(P.nq) ? ld_keep_f64(P.wt_w + c[u][a], keep) : 0.0;
         }
 #pragma unroll
         for (int u = 0; u < U; ++u)
@@ -212,52 +214,62 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
     if (threadIdx.x == 0) s_tn = 0;
     __syncthreads();
     const int64_t k0 = int64_t(blockIdx.x) * P.chunk, k1 = min(P.nme, k0 + P.chunk);
+    const unsigned nq32 = unsigned(P.nq), v032 = unsigned(P.v0), nv32 = unsigned(P.v1 - P.v0);
     constexpr int U = 4;  // triangles per thread per iteration; the next iteration's are loaded
                           // while these are counted
     int nx[U][3];
+    const unsigned nk = unsigned(k1 - k0);  // (a block's chunk is far below 2^31 triangles)
+    const int32_t* meb = P.me + 3 * k0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-        const int64_t k = k0 + threadIdx.x + u * PLACE_THREADS;
-        if (k < k1) load_tri_ids(P.me, k, nx[u][0], nx[u][1], nx[u][2]);
+        const unsigned j = threadIdx.x + u * PLACE_THREADS;
+        if (j < nk) load_tri_ids(meb, j, nx[u][0], nx[u][1], nx[u][2]);
     }
-    for (int64_t k0u = k0 + threadIdx.x; k0u < k1; k0u += U * PLACE_THREADS) {
+    for (unsigned j0 = threadIdx.x; j0 < nk; j0 += U * PLACE_THREADS) {
         int c[U][3];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             c[u][0] = nx[u][0];
             c[u][1] = nx[u][1];
             c[u][2] = nx[u][2];
-            const int64_t k = k0u + (U + u) * PLACE_THREADS;
-            if (k < k1) load_tri_ids(P.me, k, nx[u][0], nx[u][1], nx[u][2]);
+            const unsigned j = j0 + (U + u) * PLACE_THREADS;
+            if (j < nk) load_tri_ids(meb, j, nx[u][0], nx[u][1], nx[u][2]);
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
-            const int64_t k = k0u + u * PLACE_THREADS;
-            if (k >= k1) break;
-            // a triangle with an out-of-range corner is reported and left out entirely, so no
-            // incidence ever names an invalid neighbour
-            const bool ok = tri_ids_valid(c[u][0], c[u][1], c[u][2], P.nq);
-            if (P.tri && ok) {  // (same-address shared atomics of a warp are combined in hardware)
-                bool own = false;
+            const unsigned j = j0 + u * PLACE_THREADS;
+            if (j >= nk) break;
+            const int64_t k = k0 + j;
+            // a triangle with an out-of-range or repeated corner is reported (first bad position
+            // in the flattened connectivity) and left out entirely, so no incidence ever names an
+            // invalid neighbour
+            if (!tri_ids_valid(c[u][0], c[u][1], c[u][2], nq32)) {
+                if (c[u][0] == c[u][1] || c[u][1] == c[u][2] || c[u][0] == c[u][2])  // first repeating corner
+                    atomic_min_i64(&P.res->repeat_error_pos, 3 * k + (c[u][0] == c[u][1] ? 1 : 2));
 #pragma unroll
-                for (int a = 0; a < 3; ++a) own |= c[u][a] >= P.v0 && c[u][a] < P.v1;
-                if (own)
-                    P.tri[k0 + atomicAdd(&s_tn, 1u)] =
-                        make_uint4(unsigned(k), unsigned(c[u][0]), unsigned(c[u][1]), unsigned(c[u][2]));
+                for (int a = 0; a < 3; ++a)
+                    if (unsigned(c[u][a]) >= nq32) atomic_min_i64(&P.res->index_error_pos, 3 * k + a);
+                continue;
             }
-            if (c[u][0] == c[u][1] || c[u][1] == c[u][2] || c[u][0] == c[u][2])  // first repeating corner
-                atomic_min_i64(&P.res->repeat_error_pos, 3 * k + (c[u][0] == c[u][1] ? 1 : 2));
+            // owned corners: v0 <= v < v1 (<= nq) in one unsigned comparison
+            unsigned vl[3];
+            bool own[3];
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                const int64_t v = c[u][a];
-                if (v < 0 || v >= P.nq) atomic_min_i64(&P.res->index_error_pos, 3 * k + a);
-                if (ok && v >= P.v0 && v < P.v1) {
-                    const unsigned vl = unsigned(v - P.v0);
+                vl[a] = unsigned(c[u][a]) - v032;
+                own[a] = vl[a] < nv32;
+            }
+            if (P.tri && (own[0] || own[1] || own[2]))  // (same-address shared atomics of a warp are combined in hardware)
+                P.tri[k0 + atomicAdd(&s_tn, 1u)] =
+                    make_uint4(unsigned(k), unsigned(c[u][0]), unsigned(c[u][1]), unsigned(c[u][2]));
+#pragma unroll
+            for (int a = 0; a < 3; ++a) {
+                if (own[a]) {
                     if (fs) {
-                        hist_fine16(s_cnt, P.part_off_f, s_cwrap, vl >> P.plog_f, P.plog - P.plog_f);
+                        hist_fine16(s_cnt, P.part_off_f, s_cwrap, vl[a] >> P.plog_f, P.plog - P.plog_f);
                     } else {
-                        atomicAdd(&s_cnt[vl >> P.plog], 1u);
-                        if (P.fine_global) atomicAdd(&P.part_off_f[vl >> P.plog_f], 1u);
+                        atomicAdd(&s_cnt[vl[a] >> P.plog], 1u);
+                        if (P.fine_global) atomicAdd(&P.part_off_f[vl[a] >> P.plog_f], 1u);
                     }
                 }
             }
@@ -294,30 +306,55 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
 // K2: exclusive scan of the part counts (one block, any part count).  Two-level plans with
 // fine counts (K1 fine_hist): the fine offsets, the split cursors, and the coarse offsets and
 // placement cursors taken at the coarse boundaries.
-__global__ void __launch_bounds__(PLAN_THREADS) k_part_scan(const __grid_constant__ PlanArgs P) {
+// Tiles of PLAN_THREADS * per counts (per <= SCAN_PER, from the launch: small plans take one
+// count per thread) go through shared memory: coalesced in, each thread scans its `per`
+// consecutive counts, coalesced out.
+constexpr int SCAN_PER = 32;
+static int scan_per(int n) { return std::max(1, std::min(SCAN_PER, (n + PLAN_THREADS - 1) / PLAN_THREADS)); }
+static size_t scan_smem_bytes(int per) { return sizeof(unsigned) * size_t(PLAN_THREADS * per + (PLAN_THREADS * per) / 32); }
+__global__ void __launch_bounds__(PLAN_THREADS) k_part_scan(const __grid_constant__ PlanArgs P, int per) {
     pdl_enter();
+    extern __shared__ unsigned s_tile[];  // [tile + tile / 32]: index i at i + i / 32 (conflict-free for per = 32)
+    const int SCAN_TILE = PLAN_THREADS * per;
     __shared__ unsigned s_warp[PLAN_THREADS / 32];
     __shared__ unsigned s_total;
     unsigned* cnt = P.fine_hist ? P.part_off_f : P.part_off;
+    unsigned* fill = P.fine_hist ? P.fine_fill : P.part_fill;
     const int n = P.fine_hist ? P.nparts_f : P.nparts;
-    const int per = (n + PLAN_THREADS - 1) / PLAN_THREADS;
-    const int i0 = threadIdx.x * per, i1 = min(n, i0 + per);
-    unsigned run = 0;
-    for (int i = i0; i < i1; ++i) run += cnt[i];
-    unsigned ex = block_exclusive_scan<PLAN_THREADS>(run, s_warp, &s_total);
-    for (int i = i0; i < i1; ++i) {
-        const unsigned c = cnt[i];
-        cnt[i] = ex;
-        if (P.fine_hist) P.fine_fill[i] = ex;
-        else P.part_fill[i] = ex;
-        ex += c;
+    const int tid = threadIdx.x;
+    unsigned carry = 0;
+    for (int base = 0; base < n; base += SCAN_TILE) {
+        const int m = min(SCAN_TILE, n - base);
+        for (int i = tid; i < m; i += PLAN_THREADS) s_tile[i + (i >> 5)] = cnt[base + i];
+        __syncthreads();
+        // thread t owns counts [per t, per t + per) of the tile
+        const int i0 = tid * per;
+        unsigned run = 0;
+        for (int j = 0; j < per; ++j) run += i0 + j < m ? s_tile[i0 + j + ((i0 + j) >> 5)] : 0u;
+        unsigned ex = carry + block_exclusive_scan<PLAN_THREADS>(run, s_warp, &s_total);
+        for (int j = 0; j < per; ++j) {
+            if (i0 + j < m) {
+                const int at = i0 + j + ((i0 + j) >> 5);
+                const unsigned c = s_tile[at];
+                s_tile[at] = ex;
+                ex += c;
+            }
+        }
+        __syncthreads();
+        for (int i = tid; i < m; i += PLAN_THREADS) {
+            const unsigned o = s_tile[i + (i >> 5)];
+            cnt[base + i] = o;
+            fill[base + i] = o;
+        }
+        carry += s_total;
+        __syncthreads();  // the tile and s_total are reused
     }
-    if (threadIdx.x == 0) cnt[n] = s_total;
+    if (tid == 0) cnt[n] = carry;
     if (!P.fine_hist) return;
     __syncthreads();  // fine offsets visible to the block
     const int F = 1 << (P.plog - P.plog_f);
-    for (int pc = threadIdx.x; pc <= P.nparts; pc += PLAN_THREADS) {
-        const unsigned o = pc < P.nparts ? cnt[pc * F] : s_total;
+    for (int pc = tid; pc <= P.nparts; pc += PLAN_THREADS) {
+        const unsigned o = pc < P.nparts ? cnt[pc * F] : carry;
         P.part_off[pc] = o;
         if (pc < P.nparts) P.part_fill[pc] = o;
     }
@@ -351,16 +388,19 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
     }
     // this block's triangles: its chunk of the mesh, or (row blocks) the ones K1 compacted
     const bool cmp = P.tri != nullptr;
-    const int64_t nj = cmp ? int64_t(P.tri_cnt[blockIdx.x]) : kb1 - kb0;
-    auto fetch = [&](int64_t j, unsigned& k, int (&c)[3]) {
+    const unsigned nj = cmp ? P.tri_cnt[blockIdx.x] : unsigned(kb1 - kb0);  // (a chunk is far below 2^31 triangles)
+    const int32_t* meb = P.me + 3 * kb0;
+    const uint4* trib = cmp ? P.tri + kb0 : nullptr;
+    const unsigned kb032 = unsigned(kb0);  // triangle ids fit 30 bits (fa_plan_create)
+    auto fetch = [&](unsigned j, unsigned& k, int (&c)[3]) {
         c[0] = c[1] = c[2] = -1;
         if (j >= nj) return;
         if (cmp) {
-            const uint4 t = P.tri[kb0 + j];
+            const uint4 t = trib[j];
             k = t.x; c[0] = int(t.y); c[1] = int(t.z); c[2] = int(t.w);
         } else {
-            k = unsigned(kb0 + j);
-            load_tri_ids(P.me, kb0 + j, c[0], c[1], c[2]);
+            k = kb032 + j;
+            load_tri_ids(meb, j, c[0], c[1], c[2]);
         }
     };
     // triangle ids of the next round are loaded while the current one is placed
@@ -368,7 +408,7 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
     unsigned nk[TPT];
 #pragma unroll
     for (int t = 0; t < TPT; ++t) fetch(t * PLACE_THREADS + tid, nk[t], nxt[t]);
-    for (int64_t r0 = 0; r0 < nj; r0 += PLACE_TRI) {
+    for (unsigned r0 = 0; r0 < nj; r0 += PLACE_TRI) {
         int cur[TPT][3];
         unsigned ck[TPT];
 #pragma unroll
@@ -386,14 +426,13 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
         for (int t = 0; t < TPT; ++t) {
             const unsigned k = ck[t];
             const int c[3] = {cur[t][0], cur[t][1], cur[t][2]};
-            const bool ok = tri_ids_valid(c[0], c[1], c[2], P.nq);  // as k_part_hist (-1: no triangle)
+            const bool ok = tri_ids_valid(c[0], c[1], c[2], unsigned(P.nq));  // as k_part_hist (-1: no triangle)
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
-                const int64_t v = c[a];
                 const int j = 3 * t + a;
                 part[j] = 0xffffffffu;
-                if (ok && v >= P.v0 && v < P.v1) {
-                    const unsigned vl = unsigned(v - P.v0);
+                const unsigned vl = unsigned(c[a]) - unsigned(P.v0);  // owned: v0 <= v < v1 (<= nq)
+                if (ok && vl < unsigned(P.v1 - P.v0)) {
                     part[j] = vl >> P.plog;
                     rank[j] = atomicAdd(&s_cnt[part[j]], 1u);
                     rec[j] = make_uint4(unsigned(k), (vl << 2) | unsigned(a),
@@ -1995,7 +2034,9 @@ static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* s
     const size_t hist_smem = sizeof(unsigned) * (P.fine_hist && !P.fine_global ? (p->nparts + 1) / 2 : p->nparts_c);
     FA_CUDA(cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_smem)));
     FA_CUDA(launch_pdl(pdl ? 1 : -1, k_part_hist, dim3(p->nblk_place), dim3(PLACE_THREADS), hist_smem, st, P));
-    FA_CUDA(launch_pdl(pdl ? 2 : -1, k_part_scan, dim3(1), dim3(PLAN_THREADS), 0, st, P));
+    const int sper = scan_per(P.fine_hist ? p->nparts : p->nparts_c);
+    FA_CUDA(cudaFuncSetAttribute(k_part_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, int(scan_smem_bytes(SCAN_PER))));
+    FA_CUDA(launch_pdl(pdl ? 2 : -1, k_part_scan, dim3(1), dim3(PLAN_THREADS), scan_smem_bytes(sper), st, P, sper));
     const size_t place_smem = place_smem_bytes(p->nparts_c);
     FA_CUDA(cudaFuncSetAttribute(k_part_place, cudaFuncAttributeMaxDynamicSharedMemorySize, int(place_smem)));
     FA_CUDA(launch_pdl(pdl ? 3 : -1, k_part_place, dim3(p->nblk_place), dim3(PLACE_THREADS), place_smem, st, P));
