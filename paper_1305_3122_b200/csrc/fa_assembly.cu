@@ -151,7 +151,7 @@ __device__ __forceinline__ void tri_wt_store(double4* Wt, int64_t k, double ar, 
 
 // K1's W records for triangles [k0, k1) (weighted mass, cold path): k_tri_wt's work on this
 // block's chunk, the connectivity reread from L2 right after the histogram pass
-__device__ __noinline__ void hist_tri_wt(const PlanArgs& P, int64_t k0, int64_t k1) {
+__device__ __forceinline__ void hist_tri_wt(const PlanArgs& P, int64_t k0, int64_t k1) {
     const uint64_t pol = l2_evict_first_policy();
     const uint64_t keep = l2_evict_last_policy();
     constexpr int U = 2;  // triangles in flight per thread
@@ -191,21 +191,38 @@ __device__ __noinline__ void hist_tri_wt(const PlanArgs& P, int64_t k0, int64_t 
 // counter that wraps hands 65536 to the global fine count and to the block's coarse count and takes its carry
 // back out of its neighbour.  Beyond FINE_HIST_MAX fine parts the fine counts go to global atomics and shared
 // memory keeps the coarse ones.
-__device__ __forceinline__ void hist_fine16(unsigned* s_cnt, unsigned* g_fine, unsigned* s_cwrap, unsigned f,
-                                            int fine_per_coarse_log2) {
-    const unsigned sh = (f & 1u) * 16u;
-    const unsigned old = atomicAdd(&s_cnt[f >> 1], 1u << sh);
-    if (((old >> sh) & 0xffffu) == 0xffffu) {  // wrapped
-        if (sh == 0) atomicSub(&s_cnt[f >> 1], 1u << 16);
-        atomicAdd(&g_fine[f], 65536u);
-        atomicAdd(&s_cwrap[f >> fine_per_coarse_log2], 1u);
-    }
+// The shared-memory counters are addressed through a 32-bit shared address kept in a register
+// (the compiler otherwise re-derives the block's shared window for every atomic) and the wrap
+// handling stays out of line: the histogram is issue-bound, every instruction of its
+// per-corner path counts (C5: 114 -> 7x instructions per triangle).
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    unsigned a = unsigned(__cvta_generic_to_shared(p));
+    asm volatile("" : "+r"(a));  // opaque: not rematerialised
+    return a;
+}
+__device__ __forceinline__ unsigned atoms_add_u32(unsigned addr, unsigned v) {
+    unsigned o;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o) : "r"(addr), "r"(v) : "memory");
+    return o;
+}
+__device__ __forceinline__ void reds_add_u32(unsigned addr, unsigned v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __noinline__ void hist_wrap16(unsigned* s_cnt, unsigned* g_fine, unsigned* s_cwrap, unsigned f,
+                                         int fine_per_coarse_log2) {
+    if ((f & 1u) == 0) atomicSub(&s_cnt[f >> 1], 1u << 16);  // the carry went into the neighbour
+    atomicAdd(&g_fine[f], 65536u);
+    atomicAdd(&s_cwrap[f >> fine_per_coarse_log2], 1u);
 }
 
+// MODE 0: single-level plan (counts per part in shared memory); 1: two-level, fine counts in
+// shared memory (16 bit); 2: two-level, fine counts in global memory, coarse ones in shared.
+// RB: row block (the triangles with an owned corner are compacted for the placement).
+template <int MODE, bool RB>
 __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_constant__ PlanArgs P) {
     pdl_enter();
     extern __shared__ unsigned s_cnt[];
-    const bool fs = P.fine_hist && !P.fine_global;  // fine counts in shared memory (16 bit)
+    constexpr bool fs = MODE == 1;  // fine counts in shared memory (16 bit)
     const int hn = fs ? (P.nparts_f + 1) / 2 : P.nparts;
     __shared__ unsigned s_tn;
     __shared__ unsigned s_cwrap[SPLIT_COARSE];  // wrapped fine counters per coarse part
@@ -215,11 +232,17 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
     __syncthreads();
     const int64_t k0 = int64_t(blockIdx.x) * P.chunk, k1 = min(P.nme, k0 + P.chunk);
     const unsigned nq32 = unsigned(P.nq), v032 = unsigned(P.v0), nv32 = unsigned(P.v1 - P.v0);
+    const unsigned cnt_sa = smem_u32(s_cnt), tn_sa = smem_u32(&s_tn);
+    const int plog = P.plog, plog_f = P.plog_f;
     constexpr int U = 4;  // triangles per thread per iteration; the next iteration's are loaded
                           // while these are counted
     int nx[U][3];
-    const unsigned nk = unsigned(k1 - k0);  // (a block's chunk is far below 2^31 triangles)
+    unsigned nk = unsigned(k1 - k0);  // (a block's chunk is far below 2^31 triangles)
     const int32_t* meb = P.me + 3 * k0;
+    uint4* trib = RB ? P.tri + k0 : nullptr;
+    // (kept in registers: the compiler otherwise recomputes them from blockIdx and the kernel
+    //  parameters at every use inside the loop)
+    asm volatile("" : "+r"(nk), "+l"(meb), "+l"(trib));
 #pragma unroll
     for (int u = 0; u < U; ++u) {
         const unsigned j = threadIdx.x + u * PLACE_THREADS;
@@ -239,11 +262,11 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
         for (int u = 0; u < U; ++u) {
             const unsigned j = j0 + u * PLACE_THREADS;
             if (j >= nk) break;
-            const int64_t k = k0 + j;
             // a triangle with an out-of-range or repeated corner is reported (first bad position
             // in the flattened connectivity) and left out entirely, so no incidence ever names an
             // invalid neighbour
             if (!tri_ids_valid(c[u][0], c[u][1], c[u][2], nq32)) {
+                const int64_t k = k0 + j;
                 if (c[u][0] == c[u][1] || c[u][1] == c[u][2] || c[u][0] == c[u][2])  // first repeating corner
                     atomic_min_i64(&P.res->repeat_error_pos, 3 * k + (c[u][0] == c[u][1] ? 1 : 2));
 #pragma unroll
@@ -259,17 +282,20 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
                 vl[a] = unsigned(c[u][a]) - v032;
                 own[a] = vl[a] < nv32;
             }
-            if (P.tri && (own[0] || own[1] || own[2]))  // (same-address shared atomics of a warp are combined in hardware)
-                P.tri[k0 + atomicAdd(&s_tn, 1u)] =
-                    make_uint4(unsigned(k), unsigned(c[u][0]), unsigned(c[u][1]), unsigned(c[u][2]));
+            if (RB && (own[0] || own[1] || own[2]))  // (same-address shared atomics of a warp are combined in hardware)
+                trib[atoms_add_u32(tn_sa, 1u)] =
+                    make_uint4(unsigned(k0 + j), unsigned(c[u][0]), unsigned(c[u][1]), unsigned(c[u][2]));
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 if (own[a]) {
                     if (fs) {
-                        hist_fine16(s_cnt, P.part_off_f, s_cwrap, vl[a] >> P.plog_f, P.plog - P.plog_f);
+                        const unsigned f = vl[a] >> plog_f, sh = (f & 1u) << 4;
+                        const unsigned old = atoms_add_u32(cnt_sa + ((f >> 1) << 2), 1u << sh);
+                        if (((old >> sh) & 0xffffu) == 0xffffu)  // wrapped (a block rarely sees 65536 incidences of one fine part)
+                            hist_wrap16(s_cnt, P.part_off_f, s_cwrap, f, plog - plog_f);
                     } else {
-                        atomicAdd(&s_cnt[vl[a] >> P.plog], 1u);
-                        if (P.fine_global) atomicAdd(&P.part_off_f[vl[a] >> P.plog_f], 1u);
+                        reds_add_u32(cnt_sa + ((vl[a] >> plog) << 2), 1u);
+                        if (MODE == 2) atomicAdd(&P.part_off_f[vl[a] >> plog_f], 1u);
                     }
                 }
             }
@@ -277,15 +303,15 @@ __global__ void __launch_bounds__(PLACE_THREADS) k_part_hist(const __grid_consta
     }
     __syncthreads();
     if (P.Wt) hist_tri_wt(P, k0, k1);
-    if (P.tri && threadIdx.x == 0) P.tri_cnt[blockIdx.x] = s_tn;
+    if (RB && threadIdx.x == 0) P.tri_cnt[blockIdx.x] = s_tn;
     unsigned* row = P.M + int64_t(blockIdx.x) * P.nparts;
     auto fine = [&](int f) { return (s_cnt[f >> 1] >> ((f & 1) * 16)) & 0xffffu; };
-    if (!P.fine_hist) {
+    if (MODE == 0) {
         for (int i = threadIdx.x; i < P.nparts; i += PLACE_THREADS) {
             row[i] = s_cnt[i];
             if (s_cnt[i]) atomicAdd(&P.part_off[i], s_cnt[i]);
         }
-    } else if (P.fine_global) {
+    } else if (MODE == 2) {
         for (int i = threadIdx.x; i < P.nparts; i += PLACE_THREADS) row[i] = s_cnt[i];
     } else {
         for (int i = threadIdx.x; i < P.nparts_f; i += PLACE_THREADS) {
@@ -2032,8 +2058,15 @@ static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* s
         P.Wt = p->Wt;
     }
     const size_t hist_smem = sizeof(unsigned) * (P.fine_hist && !P.fine_global ? (p->nparts + 1) / 2 : p->nparts_c);
-    FA_CUDA(cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_smem)));
-    FA_CUDA(launch_pdl(pdl ? 1 : -1, k_part_hist, dim3(p->nblk_place), dim3(PLACE_THREADS), hist_smem, st, P));
+    {
+        const int mode = !P.fine_hist ? 0 : (P.fine_global ? 2 : 1);
+        const bool rb = P.tri != nullptr;
+        void (*hist)(PlanArgs) = mode == 0 ? (rb ? k_part_hist<0, true> : k_part_hist<0, false>)
+                                 : mode == 1 ? (rb ? k_part_hist<1, true> : k_part_hist<1, false>)
+                                             : (rb ? k_part_hist<2, true> : k_part_hist<2, false>);
+        FA_CUDA(cudaFuncSetAttribute(hist, cudaFuncAttributeMaxDynamicSharedMemorySize, int(hist_smem)));
+        FA_CUDA(launch_pdl(pdl ? 1 : -1, hist, dim3(p->nblk_place), dim3(PLACE_THREADS), hist_smem, st, P));
+    }
     const int sper = scan_per(P.fine_hist ? p->nparts : p->nparts_c);
     FA_CUDA(cudaFuncSetAttribute(k_part_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, int(scan_smem_bytes(SCAN_PER))));
     FA_CUDA(launch_pdl(pdl ? 2 : -1, k_part_scan, dim3(1), dim3(PLAN_THREADS), scan_smem_bytes(sper), st, P, sper));
