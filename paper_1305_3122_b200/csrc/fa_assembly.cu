@@ -192,22 +192,8 @@ __device__ __forceinline__ void hist_tri_wt(const PlanArgs& P, int64_t k0, int64
 // back out of its neighbour.  Beyond FINE_HIST_MAX fine parts the fine counts go to global atomics and shared
 // memory keeps the coarse ones.
 // The shared-memory counters are addressed through a 32-bit shared address kept in a register
-// (the compiler otherwise re-derives the block's shared window for every atomic) and the wrap
-// handling stays out of line: the histogram is issue-bound, every instruction of its
-// per-corner path counts (C5: 114 -> 7x instructions per triangle).
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    unsigned a = unsigned(__cvta_generic_to_shared(p));
-    asm volatile("" : "+r"(a));  // opaque: not rematerialised
-    return a;
-}
-__device__ __forceinline__ unsigned atoms_add_u32(unsigned addr, unsigned v) {
-    unsigned o;
-    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o) : "r"(addr), "r"(v) : "memory");
-    return o;
-}
-__device__ __forceinline__ void reds_add_u32(unsigned addr, unsigned v) {
-    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
-}
+// (smem_u32, fa_common.cuh) and the wrap handling stays out of line: the histogram is
+// issue-bound, every instruction of its per-corner path counts.
 __device__ __noinline__ void hist_wrap16(unsigned* s_cnt, unsigned* g_fine, unsigned* s_cwrap, unsigned f,
                                          int fine_per_coarse_log2) {
     if ((f & 1u) == 0) atomicSub(&s_cnt[f >> 1], 1u << 16);  // the carry went into the neighbour
@@ -390,38 +376,48 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_part_scan(const __grid_constan
 // (count matrix row of K1, one atomic per part); per round of PLACE_TRI triangles the records
 // are ranked by part in shared memory, staged in part order and written as coalesced runs.
 // Order inside a part is arbitrary (K4 sorts).
+// Shared layout: staging [RI] uint4, part of every staged record [RI] u16, then per part the
+// round counts, the round's local starts and the global cursors - all addressed from one
+// 32-bit shared base (smem_u32).  RB: row block (the triangles K1 compacted).
+template <bool RB>
 __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_place(const __grid_constant__ PlanArgs P) {
     pdl_enter();
     extern __shared__ __align__(16) unsigned char smem_raw[];
     constexpr int RI = 3 * PLACE_TRI;                  // incidences per round
     constexpr int TPT = PLACE_TRI / PLACE_THREADS;      // triangles per thread per round
-    uint4* s_stage = reinterpret_cast<uint4*>(smem_raw);                    // [RI]
-    unsigned* s_cnt = reinterpret_cast<unsigned*>(s_stage + RI);            // [nparts] round counts
-    unsigned* s_lst = s_cnt + P.nparts;                                     // [nparts] round local starts
-    unsigned* s_gb = s_lst + P.nparts;                                      // [nparts] global cursor
-    unsigned short* s_part = reinterpret_cast<unsigned short*>(s_gb + P.nparts);  // [RI]
     __shared__ unsigned s_warp[PLACE_THREADS / 32];
     __shared__ unsigned s_total;
-    const int tid = threadIdx.x;
+    unsigned tid = threadIdx.x;
+    unsigned nparts = unsigned(P.nparts);
+    const unsigned stage_sa = smem_u32(smem_raw);              // [RI] uint4
+    const unsigned part_sa = stage_sa + RI * 16;                 // [RI] u16
+    const unsigned cnt_sa = part_sa + RI * 2;                    // [nparts] round counts
+    const unsigned lst_sa = cnt_sa + 4 * nparts;                 // [nparts] round local starts
+    const unsigned gb_sa = lst_sa + 4 * nparts;                  // [nparts] global cursors
     const int64_t kb0 = int64_t(blockIdx.x) * P.chunk, kb1 = min(P.nme, kb0 + P.chunk);
     {
         const unsigned* row = P.M + int64_t(blockIdx.x) * P.nparts;
-        for (int i = tid; i < P.nparts; i += PLACE_THREADS) {
+        for (unsigned i = tid; i < nparts; i += PLACE_THREADS) {
             const unsigned c = row[i];
-            s_gb[i] = c ? atomicAdd(&P.part_fill[i], c) : 0u;
-            s_cnt[i] = 0;
+            sts_u32(gb_sa + 4 * i, c ? atomicAdd(&P.part_fill[i], c) : 0u);
+            sts_u32(cnt_sa + 4 * i, 0u);
         }
     }
     // this block's triangles: its chunk of the mesh, or (row blocks) the ones K1 compacted
-    const bool cmp = P.tri != nullptr;
-    const unsigned nj = cmp ? P.tri_cnt[blockIdx.x] : unsigned(kb1 - kb0);  // (a chunk is far below 2^31 triangles)
+    unsigned nj = RB ? P.tri_cnt[blockIdx.x] : unsigned(kb1 - kb0);  // (a chunk is far below 2^31 triangles)
     const int32_t* meb = P.me + 3 * kb0;
-    const uint4* trib = cmp ? P.tri + kb0 : nullptr;
-    const unsigned kb032 = unsigned(kb0);  // triangle ids fit 30 bits (fa_plan_create)
+    const uint4* trib = RB ? P.tri + kb0 : nullptr;
+    unsigned kb032 = unsigned(kb0);  // triangle ids fit 30 bits (fa_plan_create)
+    unsigned nq32 = unsigned(P.nq), v032 = unsigned(P.v0), nv32 = unsigned(P.v1 - P.v0);
+    uint4* recb = P.rec;
+    // (kept in registers: the compiler otherwise recomputes them from the special registers and
+    //  the kernel parameters at every use inside the loop)
+    asm volatile("" : "+r"(tid), "+r"(nparts), "+r"(nj), "+l"(meb), "+l"(trib), "+r"(kb032), "+l"(recb));
+    const int plog = P.plog;
     auto fetch = [&](unsigned j, unsigned& k, int (&c)[3]) {
         c[0] = c[1] = c[2] = -1;
         if (j >= nj) return;
-        if (cmp) {
+        if (RB) {
             const uint4 t = trib[j];
             k = t.x; c[0] = int(t.y); c[1] = int(t.z); c[2] = int(t.w);
         } else {
@@ -452,15 +448,15 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
         for (int t = 0; t < TPT; ++t) {
             const unsigned k = ck[t];
             const int c[3] = {cur[t][0], cur[t][1], cur[t][2]};
-            const bool ok = tri_ids_valid(c[0], c[1], c[2], unsigned(P.nq));  // as k_part_hist (-1: no triangle)
+            const bool ok = tri_ids_valid(c[0], c[1], c[2], nq32);  // as k_part_hist (-1: no triangle)
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
                 const int j = 3 * t + a;
                 part[j] = 0xffffffffu;
-                const unsigned vl = unsigned(c[a]) - unsigned(P.v0);  // owned: v0 <= v < v1 (<= nq)
-                if (ok && vl < unsigned(P.v1 - P.v0)) {
-                    part[j] = vl >> P.plog;
-                    rank[j] = atomicAdd(&s_cnt[part[j]], 1u);
+                const unsigned vl = unsigned(c[a]) - v032;  // owned: v0 <= v < v1 (<= nq)
+                if (ok && vl < nv32) {
+                    part[j] = vl >> plog;
+                    rank[j] = atoms_add_u32(cnt_sa + 4 * part[j], 1u);
                     rec[j] = make_uint4(unsigned(k), (vl << 2) | unsigned(a),
                                         unsigned(sel3(a, c[1], c[2], c[0])), unsigned(sel3(a, c[2], c[0], c[1])));
                 }
@@ -468,45 +464,45 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
         }
         __syncthreads();
         // local starts: exclusive scan of the round counts over parts
-        const int per = (P.nparts + PLACE_THREADS - 1) / PLACE_THREADS;
+        const unsigned per = (nparts + PLACE_THREADS - 1) / PLACE_THREADS;
         unsigned run = 0;
-        for (int j = 0; j < per; ++j) {
-            const int i = tid * per + j;
-            run += i < P.nparts ? s_cnt[i] : 0u;
+        for (unsigned j = 0; j < per; ++j) {
+            const unsigned i = tid * per + j;
+            run += i < nparts ? lds_u32(cnt_sa + 4 * i) : 0u;
         }
         unsigned ex = block_exclusive_scan<PLACE_THREADS>(run, s_warp, &s_total);
-        for (int j = 0; j < per; ++j) {
-            const int i = tid * per + j;
-            if (i < P.nparts) {
-                s_lst[i] = ex;
-                ex += s_cnt[i];
+        for (unsigned j = 0; j < per; ++j) {
+            const unsigned i = tid * per + j;
+            if (i < nparts) {
+                sts_u32(lst_sa + 4 * i, ex);
+                ex += lds_u32(cnt_sa + 4 * i);
             }
         }
         __syncthreads();
 #pragma unroll
         for (int j = 0; j < 3 * TPT; ++j) {
             if (part[j] != 0xffffffffu) {
-                const unsigned pos = s_lst[part[j]] + rank[j];
+                const unsigned pos = lds_u32(lst_sa + 4 * part[j]) + rank[j];
                 FA_DCHECK(pos < unsigned(RI), "placement staging index");
-                s_stage[pos] = rec[j];
-                s_part[pos] = (unsigned short)part[j];
+                sts_v4(stage_sa + 16 * pos, rec[j]);
+                sts_u16(part_sa + 2 * pos, part[j]);
             }
         }
         __syncthreads();
-        const int total = int(s_total);
-        for (int i = tid; i < total; i += PLACE_THREADS) {
-            const unsigned p = s_part[i];
-            const unsigned g = s_gb[p] + (unsigned(i) - s_lst[p]);
-            const uint4 r = s_stage[i];
+        const unsigned total = s_total;
+        for (unsigned i = tid; i < total; i += PLACE_THREADS) {
+            const unsigned pp = lds_u16(part_sa + 2 * i);
+            const unsigned g = lds_u32(gb_sa + 4 * pp) + (i - lds_u32(lst_sa + 4 * pp));
+            const uint4 r = lds_v4(stage_sa + 16 * i);
             FA_DCHECK(int64_t(g) < 3 * P.nme, "placement record index");
-            asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(P.rec + g), "r"(r.x),
+            asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(recb + g), "r"(r.x),
                          "r"(r.y), "r"(r.z), "r"(r.w)
                          : "memory");
         }
         __syncthreads();
-        for (int i = tid; i < P.nparts; i += PLACE_THREADS) {  // advance the cursors, reset the counts
-            s_gb[i] += s_cnt[i];
-            s_cnt[i] = 0;
+        for (unsigned i = tid; i < nparts; i += PLACE_THREADS) {  // advance the cursors, reset the counts
+            sts_u32(gb_sa + 4 * i, lds_u32(gb_sa + 4 * i) + lds_u32(cnt_sa + 4 * i));
+            sts_u32(cnt_sa + 4 * i, 0u);
         }
     }
 }
@@ -2071,8 +2067,11 @@ static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* s
     FA_CUDA(cudaFuncSetAttribute(k_part_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, int(scan_smem_bytes(SCAN_PER))));
     FA_CUDA(launch_pdl(pdl ? 2 : -1, k_part_scan, dim3(1), dim3(PLAN_THREADS), scan_smem_bytes(sper), st, P, sper));
     const size_t place_smem = place_smem_bytes(p->nparts_c);
-    FA_CUDA(cudaFuncSetAttribute(k_part_place, cudaFuncAttributeMaxDynamicSharedMemorySize, int(place_smem)));
-    FA_CUDA(launch_pdl(pdl ? 3 : -1, k_part_place, dim3(p->nblk_place), dim3(PLACE_THREADS), place_smem, st, P));
+    {
+        void (*place)(PlanArgs) = P.tri ? k_part_place<true> : k_part_place<false>;
+        FA_CUDA(cudaFuncSetAttribute(place, cudaFuncAttributeMaxDynamicSharedMemorySize, int(place_smem)));
+        FA_CUDA(launch_pdl(pdl ? 3 : -1, place, dim3(p->nblk_place), dim3(PLACE_THREADS), place_smem, st, P));
+    }
     if (p->fine_hist) {
         constexpr int RI = SPLIT_RI;
         const size_t split_smem = size_t(RI) * (sizeof(uint4) + sizeof(unsigned short)) + sizeof(unsigned) * 3 * SPLIT2_LOCAL;

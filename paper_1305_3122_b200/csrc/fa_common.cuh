@@ -194,6 +194,46 @@ __device__ __forceinline__ void st_stream_i32x4(int* p, int x, int y, int z, int
 // allocation: they have no L1 reuse, and allocating their lines thrashes L1 (weighted-mass row
 // kernel -3 %, and it then runs faster with five blocks per SM).  Coordinates do allocate:
 // every neighbour of a row is gathered twice (as n1 of one triangle and n2 of the next).
+// Shared memory through a 32-bit shared address held in a register (smem_u32) and inline
+// ld/st/atom.shared: the compiler otherwise re-derives the block's shared window (S2UR
+// SR_CgaCtaId + ULEA + moves) at most shared accesses of the issue-bound plan kernels.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    unsigned a = unsigned(__cvta_generic_to_shared(p));
+    asm volatile("" : "+r"(a));  // opaque: not rematerialised
+    return a;
+}
+__device__ __forceinline__ unsigned atoms_add_u32(unsigned addr, unsigned v) {
+    unsigned o;
+    asm volatile("atom.shared.add.u32 %0, [%1], %2;" : "=r"(o) : "r"(addr), "r"(v) : "memory");
+    return o;
+}
+__device__ __forceinline__ void reds_add_u32(unsigned addr, unsigned v) {
+    asm volatile("red.shared.add.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned lds_u32(unsigned addr) {
+    unsigned v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_u32(unsigned addr, unsigned v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned lds_u16(unsigned addr) {
+    unsigned short v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_u16(unsigned addr, unsigned v) {
+    asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"((unsigned short)v) : "memory");
+}
+__device__ __forceinline__ uint4 lds_v4(unsigned addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr) : "memory");
+    return v;
+}
+__device__ __forceinline__ void sts_v4(unsigned addr, uint4 v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w) : "memory");
+}
 __device__ __forceinline__ uint64_t l2_evict_last_policy() {
     uint64_t p;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
