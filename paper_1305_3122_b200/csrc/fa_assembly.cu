@@ -89,6 +89,10 @@ constexpr int SPLIT_THREADS = 512;
 constexpr int SPLIT_RI = 4096;      // records per k_part_split round
 constexpr int SPLIT_MINB = 2;       // k_part_split blocks per SM
 constexpr int SPLIT2_LOCAL = SPLIT_THREADS;  // fine parts a k_part_split round ranks in shared memory
+// L2 prefetch distances of the streaming plan kernels (measured on C5 / C3: k_part_sort 1 / 2 / 3 /
+// 4 x the SM count: plan 8.03 / 8.04 / 8.21 / 8.51 ms and 530 / 539 / 554 / 561 us against 8.34 ms /
+// 545 us without; k_part_split one / two rounds ahead: 8.04 / 8.10 ms against 8.43 ms without)
+constexpr int SORT_PF_SMS = 1;   // k_part_sort: the part SORT_PF_SMS * (SM count) blocks ahead
 constexpr int SORT_CAP = 6912;     // part incidences sorted in shared memory (6.75 per vertex; 2 blocks / SM)
 
 // Resets the result block and zeroes the counters the following kernels accumulate into
@@ -139,6 +143,7 @@ struct PlanArgs {
     const double* wt_areas;
     const double* wt_w;
     double4* Wt;
+    int sort_pf;            // K4: parts ahead whose records are prefetched into L2 (the blocks resident at once)
 };
 
 // a triangle takes part only with three in-range, pairwise distinct vertex ids
@@ -547,6 +552,10 @@ __global__ void __launch_bounds__(SPLIT_THREADS, SPLIT_MINB)
                 f[u] = (r[u].y >> 2) >> plog;
             }
         }
+        {   // this block's next round -> L2 while the current one is ranked (one 128-byte line per thread)
+            const uint64_t rn = uint64_t(r0) + uint64_t(gridDim.x) * RI + unsigned(tid) * (128 / sizeof(uint4));
+            if (rn < total) prefetch_l2(rec + rn);
+        }
         unsigned fmin = 0xffffffffu;
 #pragma unroll
         for (int u = 0; u < PER; ++u) fmin = min(fmin, f[u]);
@@ -698,6 +707,12 @@ __global__ void __launch_bounds__(SORT_THREADS, 2) k_part_sort(const __grid_cons
     const int nvp = int(min(int64_t(PV), nv - vfirst));
     const unsigned off = P.part_off[p], n = P.part_off[p + 1] - off;
     const bool fast = PV == (1 << PLOG0) && n <= unsigned(SORT_CAP);
+    if (P.sort_pf > 0 && p + P.sort_pf < P.nparts) {  // a part sorted about half a generation of blocks later -> L2
+        const unsigned o2 = P.part_off[p + P.sort_pf], n2 = P.part_off[p + P.sort_pf + 1] - o2;
+        const uint4* base = P.rec + (o2 & ~7u);  // 128-byte lines
+        const unsigned lines = ((o2 & 7u) + n2 + 7u) >> 3;
+        for (unsigned l = tid; l < lines; l += SORT_THREADS) prefetch_l2(base + 8 * size_t(l));
+    }
     unsigned* s_cur = s_dyn;  // [PV]
     const uint64_t pol = l2_evict_first_policy();
     for (int i = tid; i < PV; i += SORT_THREADS) s_cur[i] = 0;
@@ -2048,7 +2063,7 @@ static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* s
     P.fine_global = p->fine_global;
     P.tri = p->tri; P.tri_cnt = p->tri_cnt;
     P.part_off_f = p->part_off; P.fine_fill = p->fine_fill;
-    P.wt_areas = wt_areas; P.wt_w = wt_w; P.Wt = nullptr;
+    P.wt_areas = wt_areas; P.wt_w = wt_w; P.Wt = nullptr; P.sort_pf = 0;
     if (wt_areas && wt_w) {
         if (!p->Wt) FA_CUDA(cudaMalloc(&p->Wt, sizeof(double4) * size_t(p->nme)));
         P.Wt = p->Wt;
@@ -2087,6 +2102,7 @@ static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* s
     P.plog = p->plog; P.nparts = p->nparts; P.part_off = p->part_off;  // sort level: fine parts
     P.rec = p->two_level ? p->rec2 : p->rec;
     const size_t sort_smem = sort_smem_bytes(p->plog);
+    P.sort_pf = SORT_PF_SMS * num_sms();
     FA_CUDA(cudaFuncSetAttribute(k_part_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, int(sort_smem)));
     FA_CUDA(launch_pdl(pdl ? 5 : -1, k_part_sort, dim3(p->nparts), dim3(SORT_THREADS), sort_smem, st, P));
     return FA_OK;
