@@ -579,7 +579,10 @@ __global__ void __launch_bounds__(SPLIT_THREADS, SPLIT_MINB)
         const unsigned c = s_cnt[tid];
         const unsigned ex = block_exclusive_scan<SPLIT_THREADS>(c, s_warp, &s_total);
         s_lst[tid] = ex;
-        if (c) s_gb[tid] = atomicAdd(&fine_fill[fb + tid], c);
+        // the range of this round in fine part fb + tid: the atomic's round trip is covered by
+        // the staging (its result is first needed by the copy-out)
+        unsigned gbv = 0;
+        if (c) gbv = atomicAdd(&fine_fill[fb + tid], c);
         __syncthreads();
 #pragma unroll
         for (int u = 0; u < PER; ++u) {
@@ -590,6 +593,7 @@ __global__ void __launch_bounds__(SPLIT_THREADS, SPLIT_MINB)
             s_stage[pos] = r[u];
             s_fp[pos] = (unsigned short)l;
         }
+        s_gb[tid] = gbv;
         __syncthreads();
         const unsigned staged = s_total;
         for (unsigned i = tid; i < staged; i += SPLIT_THREADS) {
