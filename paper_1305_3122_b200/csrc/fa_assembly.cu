@@ -916,6 +916,7 @@ struct RowsArgs {
     unsigned* read_done;    // per bucket: k_compact flag, zeroed here
     const double4* Wt;      // weighted mass: per-triangle W0..W2 (k_tri_wt)
     fa_result* res;
+    int pf_dist;            // elasticity: buckets ahead whose row starts / coordinates / plan entries go to L2 (0: none)
 };
 
 template <int KIND>
@@ -1288,6 +1289,7 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     __shared__ uint64_t s_prefix;
     __shared__ int64_t s_warp[NT / 32];
     __shared__ unsigned s_zeros;
+    __shared__ unsigned s_pf[2];
     if (threadIdx.x == 0) s_zeros = 0;  // ordered before its atomics by next_tile's barrier
 
     const int tid = threadIdx.x;
@@ -1303,6 +1305,24 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
     // registers)
     const unsigned gbase = A.ivptr[vb0];
     const int ntot = int(A.ivptr[vb0 + nvb] - gbase);
+    // elasticity (two blocks per SM: little else covers a bucket's three dependent round trips -
+    // row starts, plan entries, own coordinates): the bucket one generation of resident blocks
+    // ahead has its row starts and own coordinates brought into L2 now, its plan entries after
+    // phase a (C4 numeric 2.04 -> 2.00 ms; the scalar kinds, five blocks per SM, gain nothing)
+    const int64_t fvb0 = (b + A.pf_dist) * BV;
+    const bool pf = KIND == FA_KIND_ELASTIC && A.pf_dist > 0 && fvb0 < nvl;
+    unsigned fg0 = 0, fg1 = 0;
+    if (pf && tid < 32) {
+        if (tid == 0) {
+            fg0 = A.ivptr[fvb0];
+            fg1 = A.ivptr[fvb0 + min(int64_t(BV), nvl - fvb0)];
+        } else if (tid < 5) {
+            if (fvb0 + tid * 32 <= nvl) prefetch_l2(A.ivptr + fvb0 + tid * 32);
+        } else if (tid >= 8 && tid < 25 && A.q) {
+            const int64_t fv = A.v0 + fvb0 + (tid - 8) * 8;
+            if (fv < A.v1) prefetch_l2(A.q + fv);
+        }
+    }
     const bool overflow = ntot > CAP;
     const int n = overflow ? 0 : ntot;
     constexpr int PER = (CAP + NT - 1) / NT;
@@ -1329,6 +1349,10 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         s_oq[i] = (need_q && A.q && vv < A.v1) ? A.q[vv] : make_double2(0.0, 0.0);
     }
     __syncthreads();
+    if (pf && tid == 0) {
+        s_pf[0] = fg0;
+        s_pf[1] = fg1;
+    }
     for (int vl = tid; vl < nvb && !overflow; vl += NT)
         for (int j = s_vst[vl]; j < s_vst[vl + 1]; ++j) {
             FA_DCHECK(j < CAP, "row bucket slot");
@@ -1419,6 +1443,14 @@ __global__ void __launch_bounds__(KindTraits<KIND>::THREADS, KindTraits<KIND>::M
         }
     }
     const bool any_slow = __syncthreads_or(slow);  // also the end of phase a
+    if (pf && tid < 32) {  // the plan entries of the bucket pf_dist ahead -> L2
+        const unsigned f0 = s_pf[0] & ~31u, f1 = s_pf[1];
+        for (unsigned e = f0 + unsigned(tid) * 32u; e < f1; e += 32u * 32u) {
+            prefetch_l2(A.skey + e);
+            prefetch_l2(A.sn1 + e);
+            prefetch_l2(A.sn2 + e);
+        }
+    }
 
     int64_t zeros = 0;
     uint64_t base = 0;
@@ -1860,7 +1892,9 @@ static int launch_rows(const RowsArgs& A, int64_t nbuckets, cudaStream_t st) {
     const size_t smem = rows_smem_bytes<KIND>();
     FA_CUDA(cudaFuncSetAttribute(k_rows<KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
     if (g_timer_begin && record_timer(g_timer_begin, st) != FA_OK) return FA_ERR_CUDA;
-    FA_CUDA(launch_pdl(7, k_rows<KIND>, dim3(unsigned(nbuckets)), dim3(KindTraits<KIND>::THREADS), smem, st, A));
+    RowsArgs B = A;
+    B.pf_dist = KIND == FA_KIND_ELASTIC ? KindTraits<KIND>::MIN_BLOCKS * num_sms() : 0;
+    FA_CUDA(launch_pdl(7, k_rows<KIND>, dim3(unsigned(nbuckets)), dim3(KindTraits<KIND>::THREADS), smem, st, B));
     if (g_timer_end && record_timer(g_timer_end, st) != FA_OK) return FA_ERR_CUDA;
     return FA_OK;
 }
