@@ -19,9 +19,13 @@
 //                    staged in part order and written as coalesced runs
 //     K3b part_split (two-level plans only: more than SPLIT_MIN parts, or records larger than
 //                    L2) placement used coarse parts; rounds of records (any block) are
-//                    regrouped by fine part, one range per (round, fine part)
+//                    regrouped by fine part, one range per (round, fine part); the block's
+//                    next round is prefetched into L2
 //     K4 part_sort   per part: counting sort by vertex in shared memory, each vertex's list
-//                    ordered by k; written as SoA (k<<2|a, n1, n2) + per-vertex offsets ivptr
+//                    ordered by k; written as SoA (k<<2|a, n1, n2) + per-vertex offsets ivptr;
+//                    the records of a part sorted a little later are prefetched into L2
+//   (K1 and K3 are issue-bound: 32-bit id arithmetic, shared arrays behind a register-held
+//    32-bit shared address, loop invariants pinned in registers - fa_common.cuh smem_u32)
 //   numeric
 //     K5 rows        one block per bucket of BV vertices, ticket-ordered:
 //                    s) plan entries into shared memory in one round trip; per row the 2*deg
