@@ -385,9 +385,9 @@ __global__ void __launch_bounds__(PLAN_THREADS) k_part_scan(const __grid_constan
 // (count matrix row of K1, one atomic per part); per round of PLACE_TRI triangles the records
 // are ranked by part in shared memory, staged in part order and written as coalesced runs.
 // Order inside a part is arbitrary (K4 sorts).
-// Shared layout: staging [RI] uint4, part of every staged record [RI] u16, then per part the
-// round counts, the round's local starts and the global cursors - all addressed from one
-// 32-bit shared base (smem_u32).  RB: row block (the triangles K1 compacted).
+// Shared layout: staging [RI] uint4, then per part the round counts, the round's local starts
+// and the global cursors - all addressed from one 32-bit shared base (smem_u32); the copy-out
+// reads a staged record's part from the record itself.  RB: row block (the triangles K1 compacted).
 template <bool RB>
 __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_place(const __grid_constant__ PlanArgs P) {
     pdl_enter();
@@ -399,8 +399,7 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
     unsigned tid = threadIdx.x;
     unsigned nparts = unsigned(P.nparts);
     const unsigned stage_sa = smem_u32(smem_raw);              // [RI] uint4
-    const unsigned part_sa = stage_sa + RI * 16;                 // [RI] u16
-    const unsigned cnt_sa = part_sa + RI * 2;                    // [nparts] round counts
+    const unsigned cnt_sa = stage_sa + RI * 16;                  // [nparts] round counts
     const unsigned lst_sa = cnt_sa + 4 * nparts;                 // [nparts] round local starts
     const unsigned gb_sa = lst_sa + 4 * nparts;                  // [nparts] global cursors
     const int64_t kb0 = int64_t(blockIdx.x) * P.chunk, kb1 = min(P.nme, kb0 + P.chunk);
@@ -494,15 +493,14 @@ __global__ void __launch_bounds__(PLACE_THREADS, PLACE_BLOCKS_PER_SM) k_part_pla
                 const unsigned pos = lds_u32(lst_sa + 4 * part[j]) + rank[j];
                 FA_DCHECK(pos < unsigned(RI), "placement staging index");
                 sts_v4(stage_sa + 16 * pos, rec[j]);
-                sts_u16(part_sa + 2 * pos, part[j]);
             }
         }
         __syncthreads();
         const unsigned total = s_total;
         for (unsigned i = tid; i < total; i += PLACE_THREADS) {
-            const unsigned pp = lds_u16(part_sa + 2 * i);
-            const unsigned g = lds_u32(gb_sa + 4 * pp) + (i - lds_u32(lst_sa + 4 * pp));
             const uint4 r = lds_v4(stage_sa + 16 * i);
+            const unsigned pp = (r.y >> 2) >> plog;  // the staged record names its part
+            const unsigned g = lds_u32(gb_sa + 4 * pp) + (i - lds_u32(lst_sa + 4 * pp));
             FA_DCHECK(int64_t(g) < 3 * P.nme, "placement record index");
             asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(recb + g), "r"(r.x),
                          "r"(r.y), "r"(r.z), "r"(r.w)
@@ -533,7 +531,6 @@ __global__ void __launch_bounds__(SPLIT_THREADS, SPLIT_MINB)
     unsigned* s_cnt = reinterpret_cast<unsigned*>(s_stage + RI);             // [SPLIT2_LOCAL]
     unsigned* s_lst = s_cnt + SPLIT2_LOCAL;                                  // [SPLIT2_LOCAL]
     unsigned* s_gb = s_lst + SPLIT2_LOCAL;                                   // [SPLIT2_LOCAL]
-    unsigned short* s_fp = reinterpret_cast<unsigned short*>(s_gb + SPLIT2_LOCAL);  // [RI]
     __shared__ unsigned s_fbase, s_total;
     __shared__ unsigned s_warp[SPLIT_THREADS / 32];
     static_assert(SPLIT_THREADS == SPLIT2_LOCAL, "one local fine part per thread in the scan");
@@ -595,14 +592,13 @@ __global__ void __launch_bounds__(SPLIT_THREADS, SPLIT_MINB)
             const unsigned pos = s_lst[l] + rank[u];
             FA_DCHECK(pos < unsigned(RI), "split staging index");
             s_stage[pos] = r[u];
-            s_fp[pos] = (unsigned short)l;
         }
         s_gb[tid] = gbv;
         __syncthreads();
         const unsigned staged = s_total;
         for (unsigned i = tid; i < staged; i += SPLIT_THREADS) {
-            const unsigned l = s_fp[i];
             const uint4 v = s_stage[i];
+            const unsigned l = ((v.y >> 2) >> plog) - fb;  // the staged record names its fine part
             asm volatile("st.global.L1::no_allocate.v4.u32 [%0], {%1, %2, %3, %4};" ::"l"(rec2 + s_gb[l] + (i - s_lst[l])),
                          "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
                          : "memory");
@@ -1960,7 +1956,7 @@ static void plan_free(fa_plan* p) {
 }
 
 static size_t place_smem_bytes(int nparts) {
-    return size_t(3 * PLACE_TRI) * (sizeof(uint4) + sizeof(unsigned short)) + size_t(3) * sizeof(unsigned) * nparts;
+    return size_t(3 * PLACE_TRI) * sizeof(uint4) + size_t(3) * sizeof(unsigned) * nparts;
 }
 static size_t sort_smem_bytes(int plog) {
     const size_t pv = size_t(1) << plog;
@@ -2131,7 +2127,7 @@ static int plan_build(fa_plan* p, const int32_t* d_me, fa_result* d_res, void* s
     }
     if (p->fine_hist) {
         constexpr int RI = SPLIT_RI;
-        const size_t split_smem = size_t(RI) * (sizeof(uint4) + sizeof(unsigned short)) + sizeof(unsigned) * 3 * SPLIT2_LOCAL;
+        const size_t split_smem = size_t(RI) * sizeof(uint4) + sizeof(unsigned) * 3 * SPLIT2_LOCAL;
         FA_CUDA(cudaFuncSetAttribute(k_part_split, cudaFuncAttributeMaxDynamicSharedMemorySize, int(split_smem)));
         int nsm = 0, dev = 0;
         FA_CUDA(cudaGetDevice(&dev));
